@@ -1,0 +1,179 @@
+/*
+ * hfb200.h — C ABI of the B200-native FEM lead-field engine.
+ *
+ * One shared library (paper_1811_07717_b200/_lib/libhfb200.so) exports the
+ * entry points below.  Every pointer argument marked "device" is a CUDA device
+ * pointer on the current device; "host" pointers are ordinary host memory.
+ * `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ * No function allocates device memory: callers size the workspace with the
+ * matching *_workspace_bytes() query and pass it in.  Every function returns
+ * an hf_status; hf_last_error() gives a human-readable message for the last
+ * failure on the calling thread.
+ *
+ * Each entry point replaces one interface of the reference package
+ * `headfem` (files relative to /root/reference/pkg/src/headfem/):
+ *
+ *   hf_ldp                 solver.py:50-61     ldp(A)
+ *   hf_pcg_multi           solver.py:64-111    pcg_solve(A, b, cfg), one column per RHS
+ *                          solver.py:114-141   transfer_matrix(A, B, cfg, threads)
+ *   hf_csr_prune_*         (internal)          zero-free copy of A for the SpMM
+ *   hf_p1_blocks           fem.py:31-93        element_gradients + stiffness_blocks
+ *   hf_p1_assemble_*       fem.py:96-109       _scatter_blocks / volume_stiffness
+ *                          fem.py:197-224      assemble_A (+ electrode terms, _ground)
+ *   hf_response_matrix     leadfield.py:104-109 electrode_response: M = C - B'T, M = (M+M')/2
+ *   hf_lf_tail             leadfield.py:122-134 eeg_leadfield: L = W (G'T)'  with W = -R M^-1
+ *   hf_dense_lf            leadfield.py:230-237 eit_leadfield column blocks  W Q[p]'
+ *   hf_eit_sens            leadfield.py:179-207 _dof_sensitivities: Q[p,m,:] = T' K_m u_p
+ *
+ * See INTEGRATION.md for the ctypes binding the reference would use.
+ */
+#ifndef HFB200_H
+#define HFB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  HF_OK = 0,
+  HF_ERR_ARG = 1,          /* bad argument (shape, null pointer, unsupported width) */
+  HF_ERR_CUDA = 2,         /* CUDA runtime error (message in hf_last_error) */
+  HF_ERR_WORKSPACE = 3,    /* workspace too small */
+  HF_ERR_CAPACITY = 4,     /* a node touches more elements than the row builder supports */
+  HF_ERR_INTERNAL = 5      /* solver control did not terminate */
+} hf_status;
+
+/* Compressed sparse rows; int32 indices as scipy produces them (solver.py:55,87). */
+typedef struct {
+  int32_t n_rows;
+  int32_t n_cols;
+  int64_t nnz;
+  const int32_t* indptr;   /* device, n_rows+1 */
+  const int32_t* indices;  /* device, nnz, sorted within each row */
+  const double* val;       /* device, nnz */
+} hf_csr;
+
+/* Per-column terminal states reported by hf_pcg_multi. */
+enum {
+  HF_COL_DONE = 2,         /* converged: true residual <= tol (solver.py:94-100) */
+  HF_COL_FAILED = 3,       /* max_iter reached (solver.py:108-111) */
+  HF_COL_ZERO = 4,         /* ||b|| == 0: x = 0, 0 iterations (solver.py:75-76) */
+  HF_COL_FROZEN = 5        /* replay stopped at freeze_at[j] (best-iterate recovery) */
+};
+
+/* Version / diagnostics. */
+const char* hf_version(void);
+const char* hf_last_error(void);
+int hf_device_sm_count(int32_t* sm_count);
+
+/* ---------------------------------------------------------------- solver */
+
+/* d_i = sum_j |a_ij|  (solver.py:50-61).  zero_count is one device int32 of
+ * scratch; *n_zero_rows (host) receives the number of rows with d_i == 0 (the
+ * caller raises SingularPreconditionerError).  Synchronises `stream`. */
+int hf_ldp(const hf_csr* A, double* d, int32_t* zero_count, int32_t* n_zero_rows, void* stream);
+
+/* Zero-free copy of A used by the SpMM (explicit zeros add 0*x, an exact
+ * no-op for finite x).  Two steps: count (returns nnz of the copy on host),
+ * then fill into caller-allocated arrays.  ws: hf_csr_prune_workspace_bytes. */
+size_t hf_csr_prune_workspace_bytes(int32_t n_rows);
+int hf_csr_prune_count(const hf_csr* A, void* ws, size_t ws_bytes, int64_t* nnz_out, void* stream);
+int hf_csr_prune_fill(const hf_csr* A, void* ws, size_t ws_bytes, int32_t* indptr_out,
+                      int32_t* indices_out, double* val_out, void* stream);
+
+/* Multi-RHS LDP-PCG: kp independent column recurrences of solver.py:64-111
+ * advanced together through one CSR SpMM per iteration.
+ *   B, X       device, n x kp row-major (column j of the reference = X[:, j]);
+ *              kp in {2,4,8,16,32,64,128}; unused columns must be zero in B.
+ *   d          device, n (LDP diagonal, or ones for preconditioner="none")
+ *   freeze_at  device, kp int32, or NULL.  If given, column j stops right after
+ *              iteration freeze_at[j] (freeze_at[j] < 0: run normally) — used to
+ *              replay a failed column to its best iterate.
+ *   iters, status, best_iter  host, kp int32 each
+ *   true_res, best_res        host, kp double each
+ * Result per column: status HF_COL_*; iters = converged iteration count;
+ * true_res = ||b - A x|| / ||b|| at exit; best_res/best_iter = smallest
+ * recurrence residual seen and the iteration it occurred at. */
+size_t hf_pcg_workspace_bytes(int32_t n, int32_t kp);
+int hf_pcg_multi(const hf_csr* A, const double* d, const double* B, int32_t n, int32_t kp,
+                 double tol, int32_t max_iter, const int32_t* freeze_at, double* X,
+                 int32_t* iters, int32_t* status, double* true_res, double* best_res,
+                 int32_t* best_iter, void* ws, size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- assembly */
+
+/* Element blocks K_e[i][j] = V g_i . sigma g_j (fem.py:31-93).
+ *   nodes  device n x 3 f64;  tetra device m x 4 int32
+ *   elements  device int32 subset of size m_sub, or NULL (all m elements)
+ *   sigma  device: m_sub (sigma_cols == 1) or m_sub x 6 (sigma_cols == 6) f64 aligned
+ *          with the subset, or NULL
+ *          with sigma_cols == 0 for the uniform value sigma_scalar
+ *   blocks device m_sub x 16 + 1 f64 (row-major 4x4 per element; the trailing
+ *          slot is scratch for the flag word)
+ *   vols   device m_sub f64 (may be NULL)
+ *   flags  host int32: bit0 non-positive volume, bit1 negative scalar sigma,
+ *          bit2 non positive-definite tensor (AssemblyError in fem.py:56-67,82-83) */
+int hf_p1_blocks(const double* nodes, const int32_t* tetra, int32_t m, const int32_t* elements,
+                 int32_t m_sub, const double* sigma, int32_t sigma_cols, double sigma_scalar,
+                 double* blocks, double* vols, int32_t* flags, void* stream);
+
+/* CSR assembly of the P1 stiffness matrix with scipy's pattern (fem.py:96-102):
+ * rows/columns of every element pair, sorted, duplicates summed in a fixed
+ * (ascending element) order, explicit zeros kept.  Optional electrode contact
+ * terms (fem.py:206-211): triangle t adds ecoef[t] * [[2,1,1],[1,2,1],[1,1,2]]/12
+ * on its nodes, in triangle order, after the volume sum.  ground >= 0 deletes
+ * row/column `ground` and sets a_gg = 1 (fem.py:219-224).
+ *   step 1 (prepare): blocks (from hf_p1_blocks, m x 16), incidence lists and
+ *           row counts; writes indptr (device, n+1) and *nnz_out (host).
+ *   step 2 (fill):   writes indices (device, nnz) and val (device, nnz). */
+size_t hf_p1_assemble_workspace_bytes(int32_t n, int32_t m, int32_t n_etri);
+int hf_p1_assemble_prepare(const int32_t* tetra, int32_t n, int32_t m, const int32_t* etri,
+                           int32_t n_etri, int32_t ground, int32_t* indptr, int64_t* nnz_out,
+                           void* ws, size_t ws_bytes, void* stream);
+int hf_p1_assemble_fill(const int32_t* tetra, int32_t n, int32_t m, const double* blocks,
+                        const int32_t* etri, const double* ecoef, int32_t n_etri, int32_t ground,
+                        const int32_t* indptr, int32_t* indices, double* val, void* ws,
+                        size_t ws_bytes, void* stream);
+
+/* ---------------------------------------------------------------- lead field */
+
+/* M = C - B' T, then M = (M + M')/2 (leadfield.py:107-108).
+ *   Bt   CSR of B' (L x n) on device (row l = electrode l's nodes, ascending)
+ *   T    device n x ldt row-major (first L columns used)
+ *   Cdiag device L (C = diag(1/Z), fem.py:256);  M device L x L row-major
+ *   ws   device L x L doubles */
+int hf_response_matrix(const hf_csr* Bt, const double* T, int32_t ldt, int32_t L,
+                       const double* Cdiag, double* M, double* ws, void* stream);
+
+/* EEG lead field tail (leadfield.py:128-129):  LF = W (G' T)'  where
+ * W = -R M^-1 (L x L, device row-major) and G' is given as CSR (ncols x n,
+ * row c = source column c, <= 8 entries each).  LF device L x ncols row-major.
+ * The (G'T)' tile is gathered into shared memory and multiplied on the fp64
+ * tensor path (DMMA, mma.sync m8n8k4 f64). */
+int hf_lf_tail(const double* T, int32_t ldt, int32_t L, const hf_csr* Gt, const double* W,
+               double* LF, void* stream);
+
+/* Dense variant for the EIT Jacobian (leadfield.py:230-237):
+ * out[l, c] = sum_k W[l,k] * Qc[c, k] for c < ncols, with Qc device ncols x L
+ * row-major (i.e. out = W Qc').  out device L x ldo row-major. */
+int hf_dense_lf(const double* Qc, int32_t ncols, int32_t L, const double* W, double* out,
+                int32_t ldo, void* stream);
+
+/* EIT sensitivities Q[p, m, l] = sum_{e in dof m} sum_i T[conn_ei, l] (K_e u_e,p)_i
+ * with unit-conductivity K_e whose ground rows/columns are zeroed
+ * (leadfield.py:179-207).
+ *   dof_elems device (sum of DOF sizes) int32, dof_ptr device n_dofs+1 int32
+ *   T device n x ldt (L used), U device n x ldu (P used)
+ *   Q device P x n_dofs x L row-major */
+int hf_eit_sens(const double* nodes, const int32_t* tetra, const int32_t* dof_elems,
+                const int32_t* dof_ptr, int32_t n_dofs, int32_t ground, const double* T,
+                int32_t ldt, int32_t L, const double* U, int32_t ldu, int32_t P, double* Q,
+                void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HFB200_H */

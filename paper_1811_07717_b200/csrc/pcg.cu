@@ -1,0 +1,957 @@
+// Multi-RHS LDP-PCG for sm_100a.
+//
+// Restates solver.py:64-111 (pcg_solve) for kp right-hand sides at once: every
+// column keeps its own recurrence (alpha, beta, residual replacement, true-
+// residual confirmation, best iterate), exactly as transfer_matrix runs them
+// one by one (solver.py:114-141); the columns only share the matrix stream.
+//
+// Layout: every n-vector block (X, R, P, Q, B) is n x kp row-major, so the kp
+// values of one mesh node are contiguous (one 128-byte line per 16 columns).
+// A row group of LPR lanes owns one mesh node; each lane owns CPL consecutive
+// columns and moves them as double2.
+//
+// One PCG round is three kernels (and three grid-wide reductions):
+//   k_spmm_pq   q = A p                      , partial p.q   -> alpha
+//   k_update_r  r -= alpha q                 , partial r.r, r.(r/d) -> res, beta, state
+//   k_update_xp x += alpha p ; p = r/d + beta p
+// which is 80 bytes per node per column per iteration of vector traffic plus
+// one CSR read per round.  The x update is deferred to the
+// third kernel so x, p and r are each read once.
+//
+// Columns whose recurrence residual drops below tol freeze in state CHECK; at
+// the end of every chunk of rounds the check path computes b - A x for them
+// (k_spmm_resid), and either finishes the column or replaces r and resumes it
+// (k_replace + k_update_xp), exactly as solver.py:94-102.  Freezing a column
+// never changes its arithmetic, only when it is scheduled.
+//
+// Reductions are deterministic: fixed row->block mapping, fixed in-block tree,
+// and the last block to finish sums the per-block partials in block order.
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "common.cuh"
+
+namespace hf {
+namespace pcg {
+
+constexpr int BLOCK = 512;
+constexpr int NWARP = BLOCK / 32;
+constexpr int BLOCKS_PER_SM = 2;
+constexpr int CHUNK = 8;  // PCG rounds per captured graph
+
+enum : int {
+  S_RUN = 0,
+  S_CHECK = 1,
+  S_DONE = HF_COL_DONE,
+  S_FAILED = HF_COL_FAILED,
+  S_ZERO = HF_COL_ZERO,
+  S_FROZEN = HF_COL_FROZEN,
+  S_REPLACE = 6
+};
+
+// summary[] slots
+enum : int { SUM_RUN = 0, SUM_CHECK = 1, SUM_REPLACE = 2, SUM_MASKED = 3, SUM_N = 8 };
+
+struct Ctl {
+  int n, kp, G;
+  double tol;
+  int max_iter;
+  double *normb, *rz, *alpha, *beta, *best_res, *true_res;
+  int *iters, *best_iter, *state, *xmask, *pmask, *freeze;
+  double *part0, *part1;
+  unsigned int* counter;
+  int* summary;
+};
+
+struct Csr {
+  const int32_t* __restrict__ indptr;
+  const int32_t* __restrict__ indices;
+  const double* __restrict__ val;
+};
+
+template <int KP>
+struct Map {
+  static constexpr int LPR = (KP / 2 < 32) ? KP / 2 : 32;  // lanes per row
+  static constexpr int CPL = KP / LPR;                      // columns per lane (2 or 4)
+  static constexpr int RB = BLOCK / LPR;                    // rows per block pass
+  static constexpr int SPLIT = BLOCK / KP;                  // last-block reduction splits
+  static constexpr int RED = (NWARP * KP > BLOCK) ? NWARP * KP : BLOCK;
+};
+
+__host__ __device__ inline int rows_per_block(int n, int G) { return (n + G - 1) / G; }
+
+template <int CPL>
+__device__ __forceinline__ void ld_cols(const double* __restrict__ p, double (&v)[CPL]) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int h = 0; h < CPL / 2; ++h) {
+    double2 t = q[h];
+    v[2 * h] = t.x;
+    v[2 * h + 1] = t.y;
+  }
+}
+template <int CPL>
+__device__ __forceinline__ void ldg_cols(const double* __restrict__ p, double (&v)[CPL]) {
+  const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+  for (int h = 0; h < CPL / 2; ++h) {
+    double2 t = __ldg(q + h);
+    v[2 * h] = t.x;
+    v[2 * h + 1] = t.y;
+  }
+}
+template <int CPL>
+__device__ __forceinline__ void st_cols(double* p, const double (&v)[CPL]) {
+  double2* q = reinterpret_cast<double2*>(p);
+#pragma unroll
+  for (int h = 0; h < CPL / 2; ++h) q[h] = make_double2(v[2 * h], v[2 * h + 1]);
+}
+
+// Sum NV per-column values over the block in a fixed order and store the
+// block's partial row (KP values per quantity) at part[nv][blockIdx.x*KP].
+template <int KP, int NV>
+__device__ __forceinline__ void block_partials(double (&v)[NV][Map<KP>::CPL], double* sm,
+                                               double* part0, double* part1) {
+  using M = Map<KP>;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int glane = tid % M::LPR;
+#pragma unroll
+  for (int q = 0; q < NV; ++q)
+#pragma unroll
+    for (int c = 0; c < M::CPL; ++c) {
+      double x = v[q][c];
+#pragma unroll
+      for (int off = 16; off >= M::LPR; off >>= 1) x += __shfl_xor_sync(FULL, x, off);
+      v[q][c] = x;
+    }
+  if (lane < M::LPR) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q)
+#pragma unroll
+      for (int c = 0; c < M::CPL; ++c) sm[(q * NWARP + warp) * KP + glane * M::CPL + c] = v[q][c];
+  }
+  __syncthreads();
+  for (int col = tid; col < KP; col += BLOCK) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double s = 0.0;
+      for (int w = 0; w < NWARP; ++w) s += sm[(q * NWARP + w) * KP + col];
+      (q == 0 ? part0 : part1)[(size_t)blockIdx.x * KP + col] = s;
+    }
+  }
+}
+
+// Last-block detection; the last block reduces the partials of every block in
+// block order into tot[q*KP + col] (shared memory).  Returns true in the last block.
+template <int KP, int NV>
+__device__ __forceinline__ bool last_block_reduce(const Ctl& c, double* sm, double* tot) {
+  using M = Map<KP>;
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(c.counter, 1u) == (unsigned)(c.G - 1));
+  __syncthreads();
+  if (!s_last) return false;
+  __threadfence();
+  const int tid = threadIdx.x;
+  const int col = tid % KP, sp = tid / KP;
+  const int per = (c.G + M::SPLIT - 1) / M::SPLIT;
+  const int b0 = sp * per, b1 = min(c.G, b0 + per);
+#pragma unroll
+  for (int q = 0; q < NV; ++q) {
+    const double* part = (q == 0) ? c.part0 : c.part1;
+    double a0 = 0.0;
+    for (int b = b0; b < b1; ++b) a0 += ld_cg(part + (size_t)b * KP + col);
+    sm[(q * M::SPLIT + sp) * KP + col] = a0;
+  }
+  __syncthreads();
+  if (tid < KP) {
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+      double s = 0.0;
+      for (int k = 0; k < M::SPLIT; ++k) s += sm[(q * M::SPLIT + k) * KP + tid];
+      tot[q * KP + tid] = s;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) *c.counter = 0u;
+  return true;
+}
+
+__device__ __forceinline__ void recount(const Ctl& c, int kp) {
+  // single thread: refresh the run/check counters from the states
+  int nrun = 0, nchk = 0;
+  for (int j = 0; j < kp; ++j) {
+    nrun += (c.state[j] == S_RUN);
+    nchk += (c.state[j] == S_CHECK);
+  }
+  c.summary[SUM_RUN] = nrun;
+  c.summary[SUM_CHECK] = nchk;
+}
+
+// ---------------------------------------------------------------- init
+// x = 0; r = b; z = r/d; p = z; rz = r.z; ||b||   (solver.py:74-85)
+template <int KP>
+__global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
+    k_init(Ctl c, const double* __restrict__ B, const double* __restrict__ d, double* X,
+           double* R, double* P) {
+  using M = Map<KP>;
+  __shared__ double sm[2 * M::RED];
+  __shared__ double tot[2 * KP];
+  const int tid = threadIdx.x, gl = tid / M::LPR, glane = tid % M::LPR;
+  const int rpb = rows_per_block(c.n, c.G);
+  const int r0 = blockIdx.x * rpb, r1 = min(c.n, r0 + rpb);
+  double v[2][M::CPL];
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) v[0][k] = v[1][k] = 0.0;
+  for (int row = r0 + gl; row < r1; row += M::RB) {
+    const size_t o = (size_t)row * KP + glane * M::CPL;
+    double b[M::CPL], z[M::CPL], zero[M::CPL];
+    ld_cols<M::CPL>(B + o, b);
+    const double dd = d[row];
+#pragma unroll
+    for (int k = 0; k < M::CPL; ++k) {
+      z[k] = b[k] / dd;
+      zero[k] = 0.0;
+      v[0][k] += b[k] * b[k];
+      v[1][k] += b[k] * z[k];
+    }
+    st_cols<M::CPL>(X + o, zero);
+    st_cols<M::CPL>(R + o, b);
+    st_cols<M::CPL>(P + o, z);
+  }
+  block_partials<KP, 2>(v, sm, c.part0, c.part1);
+  if (!last_block_reduce<KP, 2>(c, sm, tot)) return;
+  if (tid < KP) {
+    const int j = tid;
+    const double nb = sqrt(tot[j]);
+    c.normb[j] = nb;
+    c.rz[j] = tot[KP + j];
+    c.alpha[j] = 0.0;
+    c.beta[j] = 0.0;
+    c.best_res[j] = 1.0;  // best = (1.0, x0, 0)   solver.py:85
+    c.best_iter[j] = 0;
+    c.iters[j] = 0;
+    c.true_res[j] = 0.0;
+    c.xmask[j] = 0;
+    c.pmask[j] = 0;
+    int st = S_RUN;
+    if (nb == 0.0)
+      st = S_ZERO;  // solver.py:75-76
+    else if (c.freeze != nullptr && c.freeze[j] == 0)
+      st = S_FROZEN;
+    c.state[j] = st;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    recount(c, KP);
+    c.summary[SUM_REPLACE] = 0;
+    c.summary[SUM_MASKED] = 0;
+  }
+}
+
+// ---------------------------------------------------------------- SpMM
+// Gathers sum_j a_ij * V[col_j, cols of this lane] for one row; the row's
+// (index, value) pairs are loaded cooperatively by the row group and broadcast
+// with shuffles.  Rows are processed in warp-uniform passes so shuffles never
+// diverge.  `act` masks columns whose value is not needed.
+template <int KP>
+__device__ __forceinline__ void row_gather(const Csr& A, const double* __restrict__ V, int row,
+                                           bool valid, bool any, double (&acc)[Map<KP>::CPL]) {
+  using M = Map<KP>;
+  const int glane = threadIdx.x % M::LPR;
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) acc[k] = 0.0;
+  int start = 0, len = 0;
+  if (valid) {
+    start = A.indptr[row];
+    len = A.indptr[row + 1] - start;
+  }
+  int maxlen = len;
+  if (M::LPR < 32) maxlen = __reduce_max_sync(FULL, (unsigned)len);
+  const double* __restrict__ Vl = V + glane * M::CPL;
+  for (int base = 0; base < maxlen; base += M::LPR) {
+    const int jj = base + glane;
+    int ci = 0;
+    double cv = 0.0;
+    if (jj < len) {
+      ci = __ldg(A.indices + start + jj);
+      cv = __ldg(A.val + start + jj);
+    }
+    const int nt = min(M::LPR, maxlen - base);
+    if (M::LPR == 1) {
+      if (jj < len && any) {
+        double p[M::CPL];
+        ldg_cols<M::CPL>(Vl + (size_t)ci * KP, p);
+#pragma unroll
+        for (int k = 0; k < M::CPL; ++k) acc[k] = fma(cv, p[k], acc[k]);
+      }
+    } else {
+#pragma unroll 8
+      for (int t = 0; t < nt; ++t) {
+        const int cc = __shfl_sync(FULL, ci, t, M::LPR);
+        const double vv = __shfl_sync(FULL, cv, t, M::LPR);
+        if (base + t < len && any) {
+          double p[M::CPL];
+          ldg_cols<M::CPL>(Vl + (size_t)cc * KP, p);
+#pragma unroll
+          for (int k = 0; k < M::CPL; ++k) acc[k] = fma(vv, p[k], acc[k]);
+        }
+      }
+    }
+  }
+}
+
+// q = A p, partial p.q, alpha = rz / p.q       (solver.py:87-88)
+template <int KP>
+__global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
+    k_spmm_pq(Ctl c, Csr A, const double* __restrict__ P, double* __restrict__ Q) {
+  using M = Map<KP>;
+  __shared__ double sm[M::RED];
+  __shared__ double tot[KP];
+  __shared__ int s_act[KP];
+  if (c.summary[SUM_RUN] == 0) return;
+  const int tid = threadIdx.x, gl = tid / M::LPR, glane = tid % M::LPR;
+  for (int j = tid; j < KP; j += BLOCK) s_act[j] = (c.state[j] == S_RUN);
+  __syncthreads();
+  bool act[M::CPL];
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) {
+    act[k] = s_act[glane * M::CPL + k];
+    any |= act[k];
+  }
+  const int rpb = rows_per_block(c.n, c.G);
+  const int r0 = blockIdx.x * rpb, r1 = min(c.n, r0 + rpb);
+  double v[1][M::CPL];
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) v[0][k] = 0.0;
+  for (int base = r0; base < r1; base += M::RB) {
+    const int row = base + gl;
+    const bool valid = row < r1;
+    double acc[M::CPL];
+    row_gather<KP>(A, P, row, valid, any, acc);
+    if (valid && any) {
+      const size_t o = (size_t)row * KP + glane * M::CPL;
+      st_cols<M::CPL>(Q + o, acc);
+      double p[M::CPL];
+      ldg_cols<M::CPL>(P + o, p);
+#pragma unroll
+      for (int k = 0; k < M::CPL; ++k)
+        if (act[k]) v[0][k] += p[k] * acc[k];
+    }
+  }
+  block_partials<KP, 1>(v, sm, c.part0, nullptr);
+  if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
+  if (tid < KP) {
+    if (c.state[tid] == S_RUN) c.alpha[tid] = c.rz[tid] / tot[tid];
+  }
+}
+
+// r -= alpha q ; res = |r|/|b| ; best ; tolerance / max_iter ; beta   (solver.py:90-106)
+template <int KP>
+__global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
+    k_update_r(Ctl c, const double* __restrict__ Q, double* R, const double* __restrict__ d) {
+  using M = Map<KP>;
+  __shared__ double sm[2 * M::RED];
+  __shared__ double tot[2 * KP];
+  __shared__ double s_alpha[KP];
+  __shared__ int s_act[KP];
+  if (c.summary[SUM_RUN] == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) c.summary[SUM_MASKED] = 0;
+    return;
+  }
+  const int tid = threadIdx.x, gl = tid / M::LPR, glane = tid % M::LPR;
+  for (int j = tid; j < KP; j += BLOCK) {
+    const int a = (c.state[j] == S_RUN);
+    s_act[j] = a;
+    s_alpha[j] = a ? c.alpha[j] : 0.0;
+  }
+  __syncthreads();
+  bool act[M::CPL];
+  double al[M::CPL];
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) {
+    act[k] = s_act[glane * M::CPL + k];
+    al[k] = s_alpha[glane * M::CPL + k];
+    any |= act[k];
+  }
+  const int rpb = rows_per_block(c.n, c.G);
+  const int r0 = blockIdx.x * rpb, r1 = min(c.n, r0 + rpb);
+  double v[2][M::CPL];
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) v[0][k] = v[1][k] = 0.0;
+  if (any) {
+    for (int row = r0 + gl; row < r1; row += M::RB) {
+      const size_t o = (size_t)row * KP + glane * M::CPL;
+      double r[M::CPL], q[M::CPL];
+      ld_cols<M::CPL>(R + o, r);
+      ld_cols<M::CPL>(Q + o, q);
+      const double dd = __ldg(d + row);
+#pragma unroll
+      for (int k = 0; k < M::CPL; ++k) {
+        if (act[k]) {
+          r[k] = r[k] - al[k] * q[k];
+          v[0][k] += r[k] * r[k];
+          v[1][k] += r[k] * (r[k] / dd);
+        }
+      }
+      st_cols<M::CPL>(R + o, r);
+    }
+  }
+  block_partials<KP, 2>(v, sm, c.part0, c.part1);
+  if (!last_block_reduce<KP, 2>(c, sm, tot)) return;
+  if (tid < KP) {
+    const int j = tid;
+    int xm = 0, pm = 0;
+    if (c.state[j] == S_RUN) {
+      const int k = c.iters[j] + 1;
+      c.iters[j] = k;
+      const double res = sqrt(tot[j]) / c.normb[j];
+      if (res < c.best_res[j]) {  // solver.py:92-93
+        c.best_res[j] = res;
+        c.best_iter[j] = k;
+      }
+      xm = 1;
+      if (c.freeze != nullptr && c.freeze[j] == k) {
+        c.state[j] = S_FROZEN;
+      } else if (res <= c.tol) {  // solver.py:94
+        c.state[j] = S_CHECK;
+      } else if (k >= c.max_iter) {  // loop exhausted, solver.py:108
+        c.state[j] = S_FAILED;
+      } else {
+        const double rzn = tot[KP + j];  // solver.py:103-106
+        c.beta[j] = rzn / c.rz[j];
+        c.rz[j] = rzn;
+        pm = 1;
+      }
+    }
+    c.xmask[j] = xm;
+    c.pmask[j] = pm;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    recount(c, KP);
+    int masked = 0;
+    for (int j = 0; j < KP; ++j) masked += c.xmask[j] | c.pmask[j];
+    c.summary[SUM_MASKED] = masked;
+  }
+}
+
+// x += alpha p (xmask) ; p = r/d + beta p (pmask)      (solver.py:89,103,107)
+template <int KP>
+__global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
+    k_update_xp(Ctl c, int gate, double* X, double* P, const double* __restrict__ R,
+                const double* __restrict__ d) {
+  using M = Map<KP>;
+  __shared__ double s_alpha[KP], s_beta[KP];
+  __shared__ int s_xm[KP], s_pm[KP];
+  if (c.summary[gate] == 0) return;
+  const int tid = threadIdx.x, gl = tid / M::LPR, glane = tid % M::LPR;
+  for (int j = tid; j < KP; j += BLOCK) {
+    s_xm[j] = c.xmask[j];
+    s_pm[j] = c.pmask[j];
+    s_alpha[j] = c.alpha[j];
+    s_beta[j] = c.beta[j];
+  }
+  __syncthreads();
+  bool xm[M::CPL], pm[M::CPL];
+  double al[M::CPL], be[M::CPL];
+  bool anyx = false, anyp = false;
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) {
+    const int j = glane * M::CPL + k;
+    xm[k] = s_xm[j];
+    pm[k] = s_pm[j];
+    al[k] = s_alpha[j];
+    be[k] = s_beta[j];
+    anyx |= xm[k];
+    anyp |= pm[k];
+  }
+  if (!anyx && !anyp) return;
+  const int rpb = rows_per_block(c.n, c.G);
+  const int r0 = blockIdx.x * rpb, r1 = min(c.n, r0 + rpb);
+  for (int row = r0 + gl; row < r1; row += M::RB) {
+    const size_t o = (size_t)row * KP + glane * M::CPL;
+    double p[M::CPL];
+    ld_cols<M::CPL>(P + o, p);
+    if (anyx) {
+      double x[M::CPL];
+      ld_cols<M::CPL>(X + o, x);
+#pragma unroll
+      for (int k = 0; k < M::CPL; ++k)
+        if (xm[k]) x[k] = x[k] + al[k] * p[k];
+      st_cols<M::CPL>(X + o, x);
+    }
+    if (anyp) {
+      double r[M::CPL];
+      ld_cols<M::CPL>(R + o, r);
+      const double dd = __ldg(d + row);
+#pragma unroll
+      for (int k = 0; k < M::CPL; ++k)
+        if (pm[k]) p[k] = r[k] / dd + be[k] * p[k];
+      st_cols<M::CPL>(P + o, p);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- check path
+// s = b - A x for CHECK columns (into Q), true residual, DONE / FAILED / REPLACE
+// (solver.py:94-102)
+template <int KP>
+__global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
+    k_spmm_resid(Ctl c, Csr A, const double* __restrict__ B, const double* __restrict__ X,
+                 double* __restrict__ Q) {
+  using M = Map<KP>;
+  __shared__ double sm[M::RED];
+  __shared__ double tot[KP];
+  __shared__ int s_act[KP];
+  if (c.summary[SUM_CHECK] == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) c.summary[SUM_REPLACE] = 0;
+    return;
+  }
+  const int tid = threadIdx.x, gl = tid / M::LPR, glane = tid % M::LPR;
+  for (int j = tid; j < KP; j += BLOCK) s_act[j] = (c.state[j] == S_CHECK);
+  __syncthreads();
+  bool act[M::CPL];
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) {
+    act[k] = s_act[glane * M::CPL + k];
+    any |= act[k];
+  }
+  const int rpb = rows_per_block(c.n, c.G);
+  const int r0 = blockIdx.x * rpb, r1 = min(c.n, r0 + rpb);
+  double v[1][M::CPL];
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) v[0][k] = 0.0;
+  for (int base = r0; base < r1; base += M::RB) {
+    const int row = base + gl;
+    const bool valid = row < r1;
+    double acc[M::CPL];
+    row_gather<KP>(A, X, row, valid, any, acc);
+    if (valid && any) {
+      const size_t o = (size_t)row * KP + glane * M::CPL;
+      double b[M::CPL], q[M::CPL];
+      ld_cols<M::CPL>(B + o, b);
+      ld_cols<M::CPL>(Q + o, q);
+#pragma unroll
+      for (int k = 0; k < M::CPL; ++k)
+        if (act[k]) {
+          q[k] = b[k] - acc[k];
+          v[0][k] += q[k] * q[k];
+        }
+      st_cols<M::CPL>(Q + o, q);
+    }
+  }
+  block_partials<KP, 1>(v, sm, c.part0, nullptr);
+  if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
+  if (tid < KP) {
+    const int j = tid;
+    if (c.state[j] == S_CHECK) {
+      const double t = sqrt(tot[j]) / c.normb[j];
+      c.true_res[j] = t;
+      if (t <= c.tol)
+        c.state[j] = S_DONE;
+      else if (c.iters[j] >= c.max_iter)
+        c.state[j] = S_FAILED;
+      else
+        c.state[j] = S_REPLACE;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int nrep = 0;
+    for (int j = 0; j < KP; ++j) nrep += (c.state[j] == S_REPLACE);
+    c.summary[SUM_REPLACE] = nrep;
+    recount(c, KP);
+  }
+}
+
+// r = s for REPLACE columns, rz_next = r.(r/d), beta, resume   (solver.py:101-106)
+template <int KP>
+__global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
+    k_replace(Ctl c, const double* __restrict__ Q, double* R, const double* __restrict__ d) {
+  using M = Map<KP>;
+  __shared__ double sm[M::RED];
+  __shared__ double tot[KP];
+  __shared__ int s_act[KP];
+  if (c.summary[SUM_REPLACE] == 0) return;
+  const int tid = threadIdx.x, gl = tid / M::LPR, glane = tid % M::LPR;
+  for (int j = tid; j < KP; j += BLOCK) s_act[j] = (c.state[j] == S_REPLACE);
+  __syncthreads();
+  bool act[M::CPL];
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) {
+    act[k] = s_act[glane * M::CPL + k];
+    any |= act[k];
+  }
+  const int rpb = rows_per_block(c.n, c.G);
+  const int r0 = blockIdx.x * rpb, r1 = min(c.n, r0 + rpb);
+  double v[1][M::CPL];
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) v[0][k] = 0.0;
+  if (any) {
+    for (int row = r0 + gl; row < r1; row += M::RB) {
+      const size_t o = (size_t)row * KP + glane * M::CPL;
+      double r[M::CPL], q[M::CPL];
+      ld_cols<M::CPL>(R + o, r);
+      ld_cols<M::CPL>(Q + o, q);
+      const double dd = __ldg(d + row);
+#pragma unroll
+      for (int k = 0; k < M::CPL; ++k)
+        if (act[k]) {
+          r[k] = q[k];
+          v[0][k] += r[k] * (r[k] / dd);
+        }
+      st_cols<M::CPL>(R + o, r);
+    }
+  }
+  block_partials<KP, 1>(v, sm, c.part0, nullptr);
+  if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
+  if (tid < KP) {
+    const int j = tid;
+    int pm = 0;
+    if (c.state[j] == S_REPLACE) {
+      const double rzn = tot[j];
+      c.beta[j] = rzn / c.rz[j];
+      c.rz[j] = rzn;
+      c.state[j] = S_RUN;
+      pm = 1;
+    }
+    c.xmask[j] = 0;
+    c.pmask[j] = pm;
+  }
+  __syncthreads();
+  if (tid == 0) recount(c, KP);
+}
+
+// ---------------------------------------------------------------- host driver
+
+inline int grid_for(int n, int kp) {
+  const int lpr = (kp / 2 < 32) ? kp / 2 : 32;
+  const int rb = BLOCK / lpr;
+  int g = sm_count() * BLOCKS_PER_SM;
+  const int need = (n + rb - 1) / rb;
+  if (need < g) g = need;
+  return g < 1 ? 1 : g;
+}
+
+struct Layout {
+  double *R, *P, *Q, *part0, *part1;
+  double *normb, *rz, *alpha, *beta, *best_res, *true_res;
+  int *iters, *best_iter, *state, *xmask, *pmask, *freeze;
+  unsigned int* counter;
+  int* summary;
+  size_t bytes;
+};
+
+inline Layout carve(void* ws, int n, int kp) {
+  Carve cv{reinterpret_cast<char*>(ws), 0, ~size_t(0)};
+  Layout L;
+  const size_t nk = (size_t)n * kp;
+  const int gmax = sm_count() * BLOCKS_PER_SM;
+  L.R = cv.take<double>(nk);
+  L.P = cv.take<double>(nk);
+  L.Q = cv.take<double>(nk);
+  L.part0 = cv.take<double>((size_t)gmax * kp);
+  L.part1 = cv.take<double>((size_t)gmax * kp);
+  L.normb = cv.take<double>(kp);
+  L.rz = cv.take<double>(kp);
+  L.alpha = cv.take<double>(kp);
+  L.beta = cv.take<double>(kp);
+  L.best_res = cv.take<double>(kp);
+  L.true_res = cv.take<double>(kp);
+  L.iters = cv.take<int>(kp);
+  L.best_iter = cv.take<int>(kp);
+  L.state = cv.take<int>(kp);
+  L.xmask = cv.take<int>(kp);
+  L.pmask = cv.take<int>(kp);
+  L.freeze = cv.take<int>(kp);
+  L.counter = cv.take<unsigned int>(4);
+  L.summary = cv.take<int>(SUM_N);
+  L.bytes = cv.used + 256;
+  return L;
+}
+
+template <int KP>
+int run(const hf_csr* A, const double* d, const double* B, int n, double tol, int max_iter,
+        const int32_t* freeze_at, double* X, int32_t* iters, int32_t* status, double* true_res,
+        double* best_res, int32_t* best_iter, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  Layout L = carve(ws, n, KP);
+  if (L.bytes > ws_bytes) {
+    set_error("pcg workspace too small: need %zu, have %zu", L.bytes, ws_bytes);
+    return HF_ERR_WORKSPACE;
+  }
+  Ctl c;
+  c.n = n;
+  c.kp = KP;
+  c.G = grid_for(n, KP);
+  c.tol = tol;
+  c.max_iter = max_iter;
+  c.normb = L.normb;
+  c.rz = L.rz;
+  c.alpha = L.alpha;
+  c.beta = L.beta;
+  c.best_res = L.best_res;
+  c.true_res = L.true_res;
+  c.iters = L.iters;
+  c.best_iter = L.best_iter;
+  c.state = L.state;
+  c.xmask = L.xmask;
+  c.pmask = L.pmask;
+  c.freeze = nullptr;
+  c.part0 = L.part0;
+  c.part1 = L.part1;
+  c.counter = L.counter;
+  c.summary = L.summary;
+  if (freeze_at != nullptr) {
+    HF_CUDA(cudaMemcpyAsync(L.freeze, freeze_at, sizeof(int) * KP, cudaMemcpyDeviceToDevice, stream));
+    c.freeze = L.freeze;
+  }
+  Csr csr{A->indptr, A->indices, A->val};
+  HF_CUDA(cudaMemsetAsync(L.counter, 0, sizeof(unsigned int) * 4, stream));
+  k_init<KP><<<c.G, BLOCK, 0, stream>>>(c, B, d, X, L.R, L.P);
+  HF_LAUNCH_CHECK();
+
+  int* h_sum = nullptr;
+  HF_CUDA(cudaHostAlloc(&h_sum, sizeof(int) * SUM_N, cudaHostAllocDefault));
+  struct Guard {
+    int* h;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    ~Guard() {
+      if (ge) cudaGraphExecDestroy(ge);
+      if (g) cudaGraphDestroy(g);
+      if (cs) cudaStreamDestroy(cs);
+      for (auto e : ev)
+        if (e) cudaEventDestroy(e);
+      if (h) cudaFreeHost(h);
+    }
+  } guard{h_sum};
+  HF_CUDA(cudaMemcpyAsync(h_sum, L.summary, sizeof(int) * SUM_N, cudaMemcpyDeviceToHost, stream));
+  HF_CUDA(cudaStreamSynchronize(stream));
+
+  if (h_sum[SUM_RUN] > 0) {
+    // Capture one chunk: CHUNK rounds, then the check path, then the status copy.
+    HF_CUDA(cudaStreamCreateWithFlags(&guard.cs, cudaStreamNonBlocking));
+    HF_CUDA(cudaStreamBeginCapture(guard.cs, cudaStreamCaptureModeThreadLocal));
+    for (int r = 0; r < CHUNK; ++r) {
+      k_spmm_pq<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, csr, L.P, L.Q);
+      k_update_r<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, L.Q, L.R, d);
+      k_update_xp<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, SUM_MASKED, X, L.P, L.R, d);
+    }
+    k_spmm_resid<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, csr, B, X, L.Q);
+    k_replace<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, L.Q, L.R, d);
+    k_update_xp<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, SUM_REPLACE, X, L.P, L.R, d);
+    cudaMemcpyAsync(h_sum, L.summary, sizeof(int) * SUM_N, cudaMemcpyDeviceToHost, guard.cs);
+    cudaError_t ce = cudaStreamEndCapture(guard.cs, &guard.g);
+    if (ce != cudaSuccess) {
+      set_error("graph capture failed: %s", cudaGetErrorString(ce));
+      return HF_ERR_CUDA;
+    }
+    HF_CUDA(cudaGraphInstantiate(&guard.ge, guard.g, 0));
+    HF_CUDA(cudaEventCreateWithFlags(&guard.ev[0], cudaEventDisableTiming));
+    HF_CUDA(cudaEventCreateWithFlags(&guard.ev[1], cudaEventDisableTiming));
+    // Every chunk costs at least one iteration of some column (or finishes a
+    // CHECK); bound the loop generously and report if control never settles.
+    const long max_chunks = 4L * (max_iter / CHUNK + 2) + 64;
+    long i = 0;
+    bool finished = false;
+    for (; i < max_chunks; ++i) {
+      HF_CUDA(cudaGraphLaunch(guard.ge, stream));
+      HF_CUDA(cudaEventRecord(guard.ev[i & 1], stream));
+      if (i >= 1) {
+        HF_CUDA(cudaEventSynchronize(guard.ev[(i - 1) & 1]));
+        volatile int* hs = h_sum;
+        if (hs[SUM_RUN] == 0 && hs[SUM_CHECK] == 0) {
+          finished = true;
+          break;
+        }
+      }
+    }
+    HF_CUDA(cudaStreamSynchronize(stream));
+    if (!finished) {
+      volatile int* hs = h_sum;
+      if (!(hs[SUM_RUN] == 0 && hs[SUM_CHECK] == 0)) {
+        set_error("pcg control did not terminate after %ld chunks", i);
+        return HF_ERR_INTERNAL;
+      }
+    }
+  }
+  // Per-column results back to the host.
+  HF_CUDA(cudaMemcpyAsync(iters, L.iters, sizeof(int) * KP, cudaMemcpyDeviceToHost, stream));
+  HF_CUDA(cudaMemcpyAsync(status, L.state, sizeof(int) * KP, cudaMemcpyDeviceToHost, stream));
+  HF_CUDA(cudaMemcpyAsync(true_res, L.true_res, sizeof(double) * KP, cudaMemcpyDeviceToHost, stream));
+  HF_CUDA(cudaMemcpyAsync(best_res, L.best_res, sizeof(double) * KP, cudaMemcpyDeviceToHost, stream));
+  HF_CUDA(cudaMemcpyAsync(best_iter, L.best_iter, sizeof(int) * KP, cudaMemcpyDeviceToHost, stream));
+  HF_CUDA(cudaStreamSynchronize(stream));
+  return HF_OK;
+}
+
+// ---------------------------------------------------------------- ldp / prune
+__global__ void k_ldp(int n, const int32_t* __restrict__ indptr, const double* __restrict__ val,
+                      double* __restrict__ d, int* __restrict__ nzero) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int j = indptr[i]; j < indptr[i + 1]; ++j) s += fabs(val[j]);  // solver.py:55
+  d[i] = s;
+  if (s == 0.0) atomicAdd(nzero, 1);
+}
+
+__global__ void k_prune_count(int n, const int32_t* __restrict__ indptr,
+                              const double* __restrict__ val, int32_t* __restrict__ cnt) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int c = 0;
+  for (int j = indptr[i]; j < indptr[i + 1]; ++j) c += (val[j] != 0.0);
+  cnt[i] = c;
+}
+
+__global__ void k_prune_fill(int n, const int32_t* __restrict__ indptr,
+                             const int32_t* __restrict__ indices, const double* __restrict__ val,
+                             const int32_t* __restrict__ off, int32_t* __restrict__ optr,
+                             int32_t* __restrict__ oidx, double* __restrict__ oval, int total) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i > n) return;
+  if (i == n) {
+    optr[n] = total;
+    return;
+  }
+  int o = off[i];
+  optr[i] = o;
+  for (int j = indptr[i]; j < indptr[i + 1]; ++j) {
+    const double v = val[j];
+    if (v != 0.0) {
+      oidx[o] = indices[j];
+      oval[o] = v;
+      ++o;
+    }
+  }
+}
+
+}  // namespace pcg
+}  // namespace hf
+
+using namespace hf;
+
+extern "C" size_t hf_pcg_workspace_bytes(int32_t n, int32_t kp) {
+  return pcg::carve(nullptr, n, kp).bytes;
+}
+
+extern "C" int hf_pcg_multi(const hf_csr* A, const double* d, const double* B, int32_t n,
+                            int32_t kp, double tol, int32_t max_iter, const int32_t* freeze_at,
+                            double* X, int32_t* iters, int32_t* status, double* true_res,
+                            double* best_res, int32_t* best_iter, void* ws, size_t ws_bytes,
+                            void* stream) {
+  if (!A || !d || !B || !X || !iters || !status || !true_res || !best_res || !best_iter || !ws) {
+    set_error("hf_pcg_multi: null argument");
+    return HF_ERR_ARG;
+  }
+  if (n <= 0 || A->n_rows != n || A->n_cols != n || max_iter < 1 || !(tol > 0.0)) {
+    set_error("hf_pcg_multi: bad shape or settings (n=%d rows=%d cols=%d max_iter=%d)", n,
+              A->n_rows, A->n_cols, max_iter);
+    return HF_ERR_ARG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+#define HF_PCG_CASE(K)                                                                         \
+  case K:                                                                                      \
+    return pcg::run<K>(A, d, B, n, tol, max_iter, freeze_at, X, iters, status, true_res,       \
+                       best_res, best_iter, ws, ws_bytes, s);
+  switch (kp) {
+    HF_PCG_CASE(2)
+    HF_PCG_CASE(4)
+    HF_PCG_CASE(8)
+    HF_PCG_CASE(16)
+    HF_PCG_CASE(32)
+    HF_PCG_CASE(64)
+    HF_PCG_CASE(128)
+    default:
+      set_error("hf_pcg_multi: unsupported column width kp=%d", kp);
+      return HF_ERR_ARG;
+  }
+#undef HF_PCG_CASE
+}
+
+extern "C" int hf_ldp(const hf_csr* A, double* d, int32_t* zero_count, int32_t* n_zero_rows,
+                      void* stream) {
+  if (!A || !d || !zero_count || !n_zero_rows) {
+    set_error("hf_ldp: null argument");
+    return HF_ERR_ARG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  HF_CUDA(cudaMemsetAsync(zero_count, 0, sizeof(int32_t), s));
+  const int n = A->n_rows;
+  if (n > 0) pcg::k_ldp<<<(n + 255) / 256, 256, 0, s>>>(n, A->indptr, A->val, d, zero_count);
+  HF_LAUNCH_CHECK();
+  int hz = 0;
+  HF_CUDA(cudaMemcpyAsync(&hz, zero_count, sizeof(int), cudaMemcpyDeviceToHost, s));
+  HF_CUDA(cudaStreamSynchronize(s));
+  *n_zero_rows = hz;
+  return HF_OK;
+}
+
+extern "C" size_t hf_csr_prune_workspace_bytes(int32_t n_rows) {
+  const size_t e = (size_t)n_rows + 1;
+  return (2 * e + scan_scratch_elems(n_rows) + 64) * sizeof(int32_t) + 1024;
+}
+
+static int prune_scan(const hf_csr* A, void* ws, size_t ws_bytes, int32_t** off_out,
+                      int32_t* total, cudaStream_t s) {
+  const int n = A->n_rows;
+  if (ws_bytes < hf_csr_prune_workspace_bytes(n)) {
+    set_error("prune workspace too small");
+    return HF_ERR_WORKSPACE;
+  }
+  Carve cv{reinterpret_cast<char*>(ws), 0, ws_bytes};
+  int32_t* cnt = cv.take<int32_t>((size_t)n + 1);
+  int32_t* off = cv.take<int32_t>((size_t)n + 1);
+  int32_t* scratch = cv.take<int32_t>(scan_scratch_elems(n));
+  int32_t* tot = cv.take<int32_t>(4);
+  pcg::k_prune_count<<<(n + 255) / 256, 256, 0, s>>>(n, A->indptr, A->val, cnt);
+  HF_LAUNCH_CHECK();
+  int rc = exclusive_scan_i32(cnt, off, n, scratch, tot, s);
+  if (rc) return rc;
+  HF_CUDA(cudaMemcpyAsync(total, tot, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  HF_CUDA(cudaStreamSynchronize(s));
+  *off_out = off;
+  return HF_OK;
+}
+
+extern "C" int hf_csr_prune_count(const hf_csr* A, void* ws, size_t ws_bytes, int64_t* nnz_out,
+                                  void* stream) {
+  if (!A || !ws || !nnz_out) {
+    set_error("hf_csr_prune_count: null argument");
+    return HF_ERR_ARG;
+  }
+  int32_t* off = nullptr;
+  int32_t total = 0;
+  int rc = prune_scan(A, ws, ws_bytes, &off, &total, reinterpret_cast<cudaStream_t>(stream));
+  if (rc) return rc;
+  *nnz_out = total;
+  return HF_OK;
+}
+
+extern "C" int hf_csr_prune_fill(const hf_csr* A, void* ws, size_t ws_bytes, int32_t* indptr_out,
+                                 int32_t* indices_out, double* val_out, void* stream) {
+  if (!A || !ws || !indptr_out) {
+    set_error("hf_csr_prune_fill: null argument");
+    return HF_ERR_ARG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int32_t* off = nullptr;
+  int32_t total = 0;
+  int rc = prune_scan(A, ws, ws_bytes, &off, &total, s);
+  if (rc) return rc;
+  const int n = A->n_rows;
+  pcg::k_prune_fill<<<(n + 256) / 256, 256, 0, s>>>(n, A->indptr, A->indices, A->val, off,
+                                                     indptr_out, indices_out, val_out, total);
+  HF_LAUNCH_CHECK();
+  return HF_OK;
+}

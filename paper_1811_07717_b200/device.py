@@ -1,0 +1,112 @@
+"""Device-resident sparse matrices and the prepared PCG operator.
+
+Buffers are torch CUDA tensors (PyTorch is only the allocator/stream layer);
+all arithmetic runs in libhfb200.so.  HBM layout:
+
+* CSR as scipy stores it: int32 indptr (n+1), int32 indices (nnz, sorted per
+  row), float64 values.  The parity copy keeps scipy's explicit zeros; the
+  SpMM runs on a zero-free copy (`PcgOperator.Ac`).
+* n-vector blocks are n x kp row-major float64 (kp columns of one node
+  contiguous), kp in {2,...,128}.
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from . import _native as N
+
+
+def device():
+    N.require_cuda()
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+class DeviceCsr:
+    """A CSR matrix in HBM (int32 indptr/indices, float64 values)."""
+
+    def __init__(self, indptr, indices, val, shape):
+        self.indptr, self.indices, self.val = indptr, indices, val
+        self.shape = (int(shape[0]), int(shape[1]))
+        self._s = N.csr_struct(self.shape[0], self.shape[1], indptr, indices, val)
+
+    @property
+    def nnz(self):
+        return int(self.indices.numel())
+
+    @property
+    def struct(self):
+        return self._s
+
+    @classmethod
+    def from_scipy(cls, M, dev=None):
+        dev = dev or device()
+        M = sp.csr_matrix(M)
+        if not M.has_sorted_indices:
+            M = M.copy()
+            M.sort_indices()
+        ip = torch.from_numpy(np.ascontiguousarray(M.indptr, dtype=np.int32)).to(dev)
+        ix = torch.from_numpy(np.ascontiguousarray(M.indices, dtype=np.int32)).to(dev)
+        vv = torch.from_numpy(np.ascontiguousarray(M.data, dtype=np.float64)).to(dev)
+        return cls(ip, ix, vv, M.shape)
+
+    def to_scipy(self):
+        return sp.csr_matrix((self.val.cpu().numpy(), self.indices.cpu().numpy(),
+                              self.indptr.cpu().numpy()), shape=self.shape)
+
+    def pruned(self):
+        """Zero-free copy (explicit zeros contribute +0*x, an exact no-op)."""
+        n = self.shape[0]
+        ws = torch.empty(N.lib.hf_csr_prune_workspace_bytes(n), dtype=torch.uint8, device=self.val.device)
+        nnz = N.C.c_int64(0)
+        st = N.stream_handle()
+        N.check("hf_csr_prune_count",
+                N.lib.hf_csr_prune_count(N.C.byref(self._s), N.ptr(ws), ws.numel(), N.C.byref(nnz), st))
+        k = int(nnz.value)
+        ip = torch.empty(n + 1, dtype=torch.int32, device=self.val.device)
+        ix = torch.empty(max(k, 1), dtype=torch.int32, device=self.val.device)[:k]
+        vv = torch.empty(max(k, 1), dtype=torch.float64, device=self.val.device)[:k]
+        N.check("hf_csr_prune_fill",
+                N.lib.hf_csr_prune_fill(N.C.byref(self._s), N.ptr(ws), ws.numel(), N.ptr(ip),
+                                        N.ptr(ix), N.ptr(vv), st))
+        return DeviceCsr(ip, ix, vv, self.shape)
+
+    def transpose_scipy(self):
+        return sp.csr_matrix(self.to_scipy().T)
+
+
+def ldp_device(A: DeviceCsr):
+    """(d, n_zero_rows) for d_i = sum_j |a_ij| (solver.py:50-61)."""
+    n = A.shape[0]
+    d = torch.empty(max(n, 1), dtype=torch.float64, device=A.val.device)[:n]
+    scratch = torch.empty(1, dtype=torch.int32, device=A.val.device)
+    nz = N.C.c_int32(0)
+    N.check("hf_ldp", N.lib.hf_ldp(N.C.byref(A.struct), N.ptr(d), N.ptr(scratch), N.C.byref(nz),
+                                   N.stream_handle()))
+    return d, int(nz.value)
+
+
+class PcgOperator:
+    """A prepared for the multi-RHS solver: parity CSR, zero-free SpMM copy and
+    the preconditioner diagonal (computed once, not once per column as
+    solver.py:77 does)."""
+
+    def __init__(self, A: DeviceCsr, preconditioner="ldp"):
+        if A.shape[0] != A.shape[1]:
+            raise ValueError("matrix must be square")
+        self.A = A
+        self.n = A.shape[0]
+        if preconditioner == "ldp":
+            self.d, self.n_zero_rows = ldp_device(A)
+        else:
+            self.d = torch.ones(self.n, dtype=torch.float64, device=A.val.device)
+            self.n_zero_rows = 0
+        self.Ac = A.pruned()
+
+
+def width_for(k):
+    for w in N.PCG_WIDTHS:
+        if w >= k:
+            return w
+    return N.PCG_WIDTHS[-1]
