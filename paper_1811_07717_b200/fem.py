@@ -38,8 +38,8 @@ class DeviceMesh:
         dev = dev or device()
         self.n = int(len(nodes))
         self.m = int(len(tetra))
-        self.nodes = torch.from_numpy(np.ascontiguousarray(nodes, dtype=np.float64)).to(dev)
-        self.tetra = torch.from_numpy(np.ascontiguousarray(tetra, dtype=np.int32)).to(dev)
+        self.nodes = torch.from_numpy(np.array(nodes, dtype=np.float64, order="C")).to(dev)
+        self.tetra = torch.from_numpy(np.array(tetra, dtype=np.int32, order="C")).to(dev)
 
     @classmethod
     def of(cls, mesh):

@@ -1,0 +1,175 @@
+"""Parity of the CUDA LDP-PCG (hf_pcg_multi through the package API) with the
+reference's golden outputs and the oracle (solver.py:50-141)."""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from tests.fixtures import load
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def eng(cuda):
+    import paper_1811_07717_b200 as e
+
+    return e
+
+
+@pytest.fixture(scope="module")
+def cases():
+    return load("solver_cases.npz")
+
+
+def random_spd(n, seed, cond=100.0):
+    rng = np.random.default_rng(seed)
+    Q, _ = np.linalg.qr(rng.normal(size=(n, n)))
+    return Q @ np.diag(np.geomspace(1.0, cond, n)) @ Q.T
+
+
+class TestLdp:
+    def test_identity(self, eng):
+        np.testing.assert_array_equal(eng.ldp(sp.eye(5, format="csr")), np.ones(5))
+
+    def test_formula(self, eng):
+        np.testing.assert_array_equal(eng.ldp(np.array([[2.0, -1.0], [-1.0, 2.0]])), [3.0, 3.0])
+
+    def test_zero_row(self, eng):
+        with pytest.raises(eng.SingularPreconditionerError):
+            eng.ldp(sp.csr_matrix(np.array([[1.0, 0.0], [0.0, 0.0]])))
+
+    def test_matches_oracle_on_mesh(self, eng):
+        import oracle
+        from tests.fixtures import csr
+
+        A = csr(load("layered_h12.npz"), "A")
+        # scipy's row sum and the kernel's sequential sum differ only in rounding
+        np.testing.assert_allclose(eng.ldp(A), oracle.ldp(A), rtol=2e-15, atol=0)
+
+
+class TestPcg:
+    @pytest.mark.parametrize("name", ["dense50", "bound40s0", "bound40s1", "bound40s2", "none60",
+                                      "ldp60"])
+    def test_golden(self, eng, cases, name):
+        A, b, x_ref = cases[f"{name}_A"], cases[f"{name}_b"], cases[f"{name}_x"]
+        it_ref, res_ref, tol, mi, pre = cases[f"{name}_meta"]
+        cfg = eng.PcgConfig(tolerance=tol, max_iterations=None if mi < 0 else int(mi),
+                            preconditioner="ldp" if pre else "none")
+        x, it, res = eng.pcg_solve(sp.csr_matrix(A), b, cfg)
+        assert abs(it - it_ref) <= 1
+        assert res <= tol
+        # both are within tol of the solution; 1e-6 is far above their gap
+        assert np.linalg.norm(x - x_ref) / np.linalg.norm(x_ref) < 1e-6
+
+    def test_identity_one_iteration(self, eng):
+        b = np.array([3.0, -1.0, 2.0])
+        x, it, res = eng.pcg_solve(sp.eye(3, format="csr"), b)
+        np.testing.assert_allclose(x, b, rtol=1e-14)
+        assert it == 1
+
+    def test_two_by_two_closed_form(self, eng):
+        A = sp.csr_matrix(np.array([[4.0, 1.0], [1.0, 3.0]]))
+        x, _, _ = eng.pcg_solve(A, np.array([1.0, 2.0]), eng.PcgConfig(tolerance=1e-14))
+        np.testing.assert_allclose(x, [1.0 / 11.0, 7.0 / 11.0], rtol=1e-12)
+
+    def test_zero_rhs(self, eng):
+        x, it, res = eng.pcg_solve(sp.eye(4, format="csr"), np.zeros(4))
+        np.testing.assert_array_equal(x, 0.0)
+        assert it == 0 and res == 0.0
+
+    def test_best_iterate_matches_reference(self, eng, cases):
+        A = cases["fail30_A"]
+        with pytest.raises(eng.ConvergenceError) as exc:
+            eng.pcg_solve(sp.csr_matrix(A), np.ones(30),
+                          eng.PcgConfig(tolerance=1e-14, max_iterations=3))
+        err = exc.value
+        res_ref, it_ref = cases["fail30_meta"]
+        assert err.iterations == 3 == it_ref
+        assert err.residual <= 1.0
+        assert abs(err.residual - res_ref) <= 1e-10 * res_ref
+        np.testing.assert_allclose(err.best_x, cases["fail30_best_x"], rtol=1e-10, atol=1e-14)
+        assert err.column is None
+
+    def test_config_validation(self, eng):
+        for kw in ({"tolerance": 0.0}, {"max_iterations": 0}, {"preconditioner": "amg"}):
+            with pytest.raises(eng.ParameterError):
+                eng.PcgConfig(**kw)
+
+
+class TestTransferMatrix:
+    def test_identity(self, eng):
+        B = sp.random(20, 4, density=0.3, random_state=7, format="csr")
+        T = eng.transfer_matrix(sp.eye(20, format="csr"), B)
+        np.testing.assert_allclose(T, B.toarray(), atol=1e-12)
+
+    def test_scaling(self, eng):
+        B = sp.random(15, 3, density=0.5, random_state=2, format="csr")
+        T = eng.transfer_matrix(2.0 * sp.eye(15, format="csr"), B, eng.PcgConfig(tolerance=1e-14))
+        np.testing.assert_allclose(T, B.toarray() / 2.0, rtol=1e-12)
+
+    def test_golden_with_zero_column(self, eng, cases):
+        A, B, T_ref = cases["tm40_A"], cases["tm40_B"], cases["tm40_T"]
+        T = eng.transfer_matrix(sp.csr_matrix(A), B, eng.PcgConfig(tolerance=1e-9))
+        assert T.flags.c_contiguous and T.shape == (40, 5)
+        np.testing.assert_array_equal(T[:, 2], 0.0)
+        for l in range(5):
+            if l == 2:
+                continue
+            assert np.linalg.norm(A @ T[:, l] - B[:, l]) / np.linalg.norm(B[:, l]) <= 1e-9
+            assert np.linalg.norm(T[:, l] - T_ref[:, l]) / np.linalg.norm(T_ref[:, l]) < 1e-6
+
+    def test_convergence_error_reports_column(self, eng):
+        A = sp.csr_matrix(random_spd(25, seed=1, cond=1e6))
+        B = sp.csr_matrix(np.ones((25, 2)))
+        with pytest.raises(eng.ConvergenceError) as exc:
+            eng.transfer_matrix(A, B, eng.PcgConfig(tolerance=1e-15, max_iterations=2))
+        assert exc.value.column == 0
+
+    def test_threads_do_not_change_result(self, eng):
+        A = sp.csr_matrix(random_spd(30, seed=8))
+        B = sp.random(30, 5, density=0.4, random_state=8, format="csr")
+        np.testing.assert_array_equal(eng.transfer_matrix(A, B, threads=1),
+                                      eng.transfer_matrix(A, B, threads=4))
+
+    def test_batch_membership_does_not_change_columns(self, eng):
+        """At a fixed SpMM width a column's iterates do not depend on the other
+        columns of its batch (the reduction tree depends only on n and kp)."""
+        from tests.fixtures import csr
+
+        fx = load("layered_h12.npz")
+        A, B = csr(fx, "A"), csr(fx, "B").toarray()
+        T_all = eng.transfer_matrix(A, B)              # 16 columns -> kp = 16
+        T_sub = eng.transfer_matrix(A, B[:, 2:13])     # 11 columns -> kp = 16
+        np.testing.assert_array_equal(T_all[:, 3], T_sub[:, 1])
+        B2 = B.copy()
+        B2[:, 5] *= 3.0                                # another column changes, column 3 does not
+        np.testing.assert_array_equal(T_all[:, 3], eng.transfer_matrix(A, B2)[:, 3])
+
+    @pytest.mark.parametrize("k", [1, 3, 16, 40, 70, 130])
+    def test_widths(self, eng, k):
+        """Every SpMM width (kp = 2..128, and the batch split) against the oracle."""
+        import oracle
+        from tests.fixtures import csr
+
+        fx = load("layered_h14_tensor.npz")
+        A = csr(fx, "A")
+        rng = np.random.default_rng(k)
+        B = rng.normal(size=(A.shape[0], k))
+        B[fx["ground"]] = 0.0
+        cfg = eng.PcgConfig(tolerance=1e-10)
+        T = eng.transfer_matrix(A, B, cfg)
+        for l in sorted({0, k // 2, k - 1}):
+            x, it, _ = oracle.pcg_solve(A, B[:, l], oracle.PcgSettings(tolerance=1e-10))
+            assert np.linalg.norm(T[:, l] - x) / np.linalg.norm(x) < 1e-7
+            assert np.linalg.norm(A @ T[:, l] - B[:, l]) / np.linalg.norm(B[:, l]) <= 1e-10
+
+    def test_iterations_match_reference_per_column(self, eng):
+        from paper_1811_07717_b200.solver import operator, rhs_block, solve_block
+        from tests.fixtures import csr
+
+        fx = load("layered_h12.npz")
+        cfg = eng.PcgConfig(tolerance=float(fx["tol"]))
+        op = operator(csr(fx, "A"), cfg)
+        _, info = solve_block(op, rhs_block(csr(fx, "B")), cfg)
+        assert np.all(np.abs(info.iterations - fx["iters"]) <= 1), (info.iterations, fx["iters"])
+        assert np.all(info.true_residual <= cfg.tolerance)
