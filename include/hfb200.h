@@ -16,11 +16,12 @@
  *   hf_ldp                 solver.py:50-61     ldp(A)
  *   hf_pcg_multi           solver.py:64-111    pcg_solve(A, b, cfg), one column per RHS
  *                          solver.py:114-141   transfer_matrix(A, B, cfg, threads)
+ *   hf_pcg_profile         (bench)             per-kernel CUDA-event timing of a PCG round
  *   hf_csr_prune_*         (internal)          zero-free copy of A for the SpMM
  *   hf_p1_blocks           fem.py:31-93        element_gradients + stiffness_blocks
  *   hf_p1_assemble_*       fem.py:96-109       _scatter_blocks / volume_stiffness
  *                          fem.py:197-224      assemble_A (+ electrode terms, _ground)
- *   hf_response_matrix     leadfield.py:104-109 electrode_response: M = C - B'T, M = (M+M')/2
+ *   hf_response_matrix     leadfield.py:104-109 electrode_response: M = C - B'T (column block)
  *   hf_lf_tail             leadfield.py:122-134 eeg_leadfield: L = W (G'T)'  with W = -R M^-1
  *   hf_dense_lf            leadfield.py:230-237 eit_leadfield column blocks  W Q[p]'
  *   hf_eit_sens            leadfield.py:179-207 _dof_sensitivities: Q[p,m,:] = T' K_m u_p
@@ -68,6 +69,8 @@ enum {
 const char* hf_version(void);
 const char* hf_last_error(void);
 int hf_device_sm_count(int32_t* sm_count);
+/* Kernels launched by this library so far (graph launches count their nodes). */
+long long hf_launch_count(void);
 
 /* ---------------------------------------------------------------- solver */
 
@@ -102,6 +105,13 @@ int hf_pcg_multi(const hf_csr* A, const double* d, const double* B, int32_t n, i
                  double tol, int32_t max_iter, const int32_t* freeze_at, double* X,
                  int32_t* iters, int32_t* status, double* true_res, double* best_res,
                  int32_t* best_iter, void* ws, size_t ws_bytes, void* stream);
+
+/* Timing probe for the roofline report: runs `rounds` PCG rounds of the same
+ * kernels as hf_pcg_multi (tolerance 0, so no column stops) and writes the
+ * average duration in ms of k_spmm_pq, k_update_r, k_update_xp (host float[3]),
+ * measured with CUDA events on `stream`.  Same workspace as hf_pcg_multi. */
+int hf_pcg_profile(const hf_csr* A, const double* d, const double* B, int32_t n, int32_t kp,
+                   int32_t rounds, double* X, float* ms3, void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------- assembly */
 
@@ -140,21 +150,24 @@ int hf_p1_assemble_fill(const int32_t* tetra, int32_t n, int32_t m, const double
 
 /* ---------------------------------------------------------------- lead field */
 
-/* M = C - B' T, then M = (M + M')/2 (leadfield.py:107-108).
+/* Raw electrode response block M[:, col0:col0+ncols] = C - B' T (leadfield.py:107;
+ * the caller symmetrises M = (M + M')/2 on the host, leadfield.py:108, after
+ * gathering the column blocks of every rank).
  *   Bt   CSR of B' (L x n) on device (row l = electrode l's nodes, ascending)
- *   T    device n x ldt row-major (first L columns used)
- *   Cdiag device L (C = diag(1/Z), fem.py:256);  M device L x L row-major
- *   ws   device L x L doubles */
-int hf_response_matrix(const hf_csr* Bt, const double* T, int32_t ldt, int32_t L,
-                       const double* Cdiag, double* M, double* ws, void* stream);
+ *   T    device n x ldt row-major holding the ncols transfer columns col0..
+ *   Cdiag device L (C = diag(1/Z), fem.py:256);  Mraw device L x ncols row-major */
+int hf_response_matrix(const hf_csr* Bt, const double* T, int32_t ldt, int32_t L, int32_t col0,
+                       int32_t ncols, const double* Cdiag, double* Mraw, void* stream);
 
-/* EEG lead field tail (leadfield.py:128-129):  LF = W (G' T)'  where
- * W = -R M^-1 (L x L, device row-major) and G' is given as CSR (ncols x n,
- * row c = source column c, <= 8 entries each).  LF device L x ncols row-major.
- * The (G'T)' tile is gathered into shared memory and multiplied on the fp64
- * tensor path (DMMA, mma.sync m8n8k4 f64). */
-int hf_lf_tail(const double* T, int32_t ldt, int32_t L, const hf_csr* Gt, const double* W,
-               double* LF, void* stream);
+/* EEG lead field tail (leadfield.py:128-129):  LF = W (G' T)'  where T holds K
+ * transfer columns (device n x ldt), W = -R M^-1 restricted to those K columns
+ * (device L x ldw row-major, L x K used) and G' is CSR (ncols x n, row c =
+ * source column c, <= 8 entries each).  LF device L x ncols row-major.  With
+ * K = L this is the whole lead field; with a column block it is one rank's
+ * partial sum.  The (G'T)' tile is gathered into shared memory and multiplied
+ * on the fp64 tensor path (DMMA, mma.sync m8n8k4 f64). */
+int hf_lf_tail(const double* T, int32_t ldt, int32_t K, const hf_csr* Gt, const double* W,
+               int32_t L, int32_t ldw, double* LF, void* stream);
 
 /* Dense variant for the EIT Jacobian (leadfield.py:230-237):
  * out[l, c] = sum_k W[l,k] * Qc[c, k] for c < ncols, with Qc device ncols x L

@@ -34,18 +34,20 @@ def _load():
         "hf_version": (C.c_char_p, []),
         "hf_last_error": (C.c_char_p, []),
         "hf_device_sm_count": (C.c_int, [C.POINTER(I32)]),
+        "hf_launch_count": (C.c_longlong, []),
         "hf_ldp": (C.c_int, [pcsr, P, P, C.POINTER(I32), P]),
         "hf_csr_prune_workspace_bytes": (SZ, [I32]),
         "hf_csr_prune_count": (C.c_int, [pcsr, P, SZ, C.POINTER(I64), P]),
         "hf_csr_prune_fill": (C.c_int, [pcsr, P, SZ, P, P, P, P]),
         "hf_pcg_workspace_bytes": (SZ, [I32, I32]),
         "hf_pcg_multi": (C.c_int, [pcsr, P, P, I32, I32, D, I32, P, P, P, P, P, P, P, P, SZ, P]),
+        "hf_pcg_profile": (C.c_int, [pcsr, P, P, I32, I32, I32, P, P, P, SZ, P]),
         "hf_p1_blocks": (C.c_int, [P, P, I32, P, I32, P, I32, D, P, P, C.POINTER(I32), P]),
         "hf_p1_assemble_workspace_bytes": (SZ, [I32, I32, I32]),
         "hf_p1_assemble_prepare": (C.c_int, [P, I32, I32, P, I32, I32, P, C.POINTER(I64), P, SZ, P]),
         "hf_p1_assemble_fill": (C.c_int, [P, I32, I32, P, P, P, I32, I32, P, P, P, P, SZ, P]),
-        "hf_response_matrix": (C.c_int, [pcsr, P, I32, I32, P, P, P, P]),
-        "hf_lf_tail": (C.c_int, [P, I32, I32, pcsr, P, P, P]),
+        "hf_response_matrix": (C.c_int, [pcsr, P, I32, I32, I32, I32, P, P, P]),
+        "hf_lf_tail": (C.c_int, [P, I32, I32, pcsr, P, I32, I32, P, P]),
         "hf_dense_lf": (C.c_int, [P, I32, I32, P, P, I32, P]),
         "hf_eit_sens": (C.c_int, [P, P, P, P, I32, I32, P, I32, I32, P, I32, I32, P, P]),
     }
@@ -59,9 +61,9 @@ def _load():
 lib = _load()
 
 # Every symbol include/hfb200.h declares (checked by tests/test_abi.py).
-EXPORTED = ("hf_version", "hf_last_error", "hf_device_sm_count", "hf_ldp",
+EXPORTED = ("hf_version", "hf_last_error", "hf_device_sm_count", "hf_launch_count", "hf_ldp",
             "hf_csr_prune_workspace_bytes", "hf_csr_prune_count", "hf_csr_prune_fill",
-            "hf_pcg_workspace_bytes", "hf_pcg_multi", "hf_p1_blocks",
+            "hf_pcg_workspace_bytes", "hf_pcg_multi", "hf_pcg_profile", "hf_p1_blocks",
             "hf_p1_assemble_workspace_bytes", "hf_p1_assemble_prepare", "hf_p1_assemble_fill",
             "hf_response_matrix", "hf_lf_tail", "hf_dense_lf", "hf_eit_sens")
 

@@ -3,11 +3,16 @@
 #include <stdarg.h>
 #include <stdio.h>
 
+#include <atomic>
+
 #include "common.cuh"
 
 namespace hf {
 
 static thread_local char g_err[1024] = "";
+static std::atomic<long> g_launches{0};
+
+void count_launches(long k) { g_launches.fetch_add(k, std::memory_order_relaxed); }
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -107,6 +112,7 @@ int exclusive_scan_i32(const int32_t* in, int32_t* out, int32_t n, int32_t* bloc
     set_error("scan: %d elements exceed the two-level limit", n);
     return HF_ERR_ARG;
   }
+  count_launches(nb > 1 ? 3 : 2);
   k_scan_tiles<<<nb, SCAN_T, 0, s>>>(in, out, n, block_sums);
   k_scan_sums<<<1, SCAN_T, 0, s>>>(block_sums, nb, total_dev);
   if (nb > 1) k_scan_add<<<(n + 255) / 256, 256, 0, s>>>(out, n, block_sums);
@@ -119,6 +125,8 @@ int exclusive_scan_i32(const int32_t* in, int32_t* out, int32_t n, int32_t* bloc
 extern "C" const char* hf_version(void) { return "hfb200 0.1.0 (sm_100a)"; }
 
 extern "C" const char* hf_last_error(void) { return hf::g_err; }
+
+extern "C" long long hf_launch_count(void) { return hf::g_launches.load(); }
 
 extern "C" int hf_device_sm_count(int32_t* out) {
   if (!out) return HF_ERR_ARG;

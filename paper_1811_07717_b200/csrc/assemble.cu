@@ -318,6 +318,7 @@ inline int build_incidence(const int32_t* conn, int width, int count, int n, int
   if (tot_entries) {
     const int g = (int)((tot_entries + 255) / 256);
     k_inc_count<<<g, 256, 0, s>>>(conn, width, count, cnt);
+    count_launches(1);
     HF_LAUNCH_CHECK();
   }
   int rc = exclusive_scan_i32(cnt, off, n, scratch, tot, s);
@@ -326,6 +327,7 @@ inline int build_incidence(const int32_t* conn, int width, int count, int n, int
     const int g = (int)((tot_entries + 255) / 256);
     k_inc_fill<<<g, 256, 0, s>>>(conn, width, count, off, cur, inc);
     k_inc_sort<<<(n + 127) / 128, 128, 0, s>>>(n, off, cnt, inc);
+    count_launches(2);
     HF_LAUNCH_CHECK();
   }
   return HF_OK;
@@ -357,6 +359,7 @@ extern "C" int hf_p1_blocks(const double* nodes, const int32_t* tetra, int32_t m
                                                        sigma_cols, sigma_scalar, blocks, vols,
                                                        dflag);
     HF_LAUNCH_CHECK();
+    count_launches(1);
   }
   int hf = 0;
   HF_CUDA(cudaMemcpyAsync(&hf, dflag, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -395,6 +398,7 @@ extern "C" int hf_p1_assemble_prepare(const int32_t* tetra, int32_t n, int32_t m
   asmb::k_row_count<<<g, asmb::ROW_WARPS * 32, 0, s>>>(n, tetra, w.eoff, w.ecnt, w.einc, ground,
                                                         w.rowcnt, w.err);
   HF_LAUNCH_CHECK();
+  count_launches(1);
   rc = exclusive_scan_i32(w.rowcnt, indptr, n, w.scratch, w.tot + 2, s);
   if (rc) return rc;
   HF_CUDA(cudaMemcpyAsync(indptr + n, w.tot + 2, sizeof(int32_t), cudaMemcpyDeviceToDevice, s));
@@ -431,6 +435,7 @@ extern "C" int hf_p1_assemble_fill(const int32_t* tetra, int32_t n, int32_t m,
       n_etri ? w.toff : nullptr, n_etri ? w.tcnt : nullptr, n_etri ? w.tinc : nullptr, ground,
       indptr, indices, val, w.err);
   HF_LAUNCH_CHECK();
+  count_launches(1);
   int32_t herr = 0;
   HF_CUDA(cudaMemcpyAsync(&herr, w.err, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
   HF_CUDA(cudaStreamSynchronize(s));

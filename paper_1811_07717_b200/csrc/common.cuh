@@ -10,6 +10,10 @@ namespace hf {
 
 void set_error(const char* fmt, ...);
 
+// Number of kernels this library has launched (graph launches count their
+// kernel nodes); bench.py reports it as gpu_launches.
+void count_launches(long k);
+
 #define HF_CUDA(x)                                                                    \
   do {                                                                                \
     cudaError_t e_ = (x);                                                             \

@@ -716,6 +716,7 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
   HF_CUDA(cudaMemsetAsync(L.counter, 0, sizeof(unsigned int) * 4, stream));
   k_init<KP><<<c.G, BLOCK, 0, stream>>>(c, B, d, X, L.R, L.P);
   HF_LAUNCH_CHECK();
+  count_launches(1);
 
   int* h_sum = nullptr;
   HF_CUDA(cudaHostAlloc(&h_sum, sizeof(int) * SUM_N, cudaHostAllocDefault));
@@ -765,6 +766,7 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
     bool finished = false;
     for (; i < max_chunks; ++i) {
       HF_CUDA(cudaGraphLaunch(guard.ge, stream));
+      count_launches(3 * CHUNK + 3);
       HF_CUDA(cudaEventRecord(guard.ev[i & 1], stream));
       if (i >= 1) {
         HF_CUDA(cudaEventSynchronize(guard.ev[(i - 1) & 1]));
@@ -791,6 +793,57 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
   HF_CUDA(cudaMemcpyAsync(best_res, L.best_res, sizeof(double) * KP, cudaMemcpyDeviceToHost, stream));
   HF_CUDA(cudaMemcpyAsync(best_iter, L.best_iter, sizeof(int) * KP, cudaMemcpyDeviceToHost, stream));
   HF_CUDA(cudaStreamSynchronize(stream));
+  return HF_OK;
+}
+
+// Per-kernel timing of `rounds` PCG rounds with CUDA events on the launch
+// stream (bench.py roofline).  tol = 0 keeps every column running.
+template <int KP>
+int profile(const hf_csr* A, const double* d, const double* B, int n, int rounds, double* X,
+            float* ms3, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  Layout L = carve(ws, n, KP);
+  if (L.bytes > ws_bytes) {
+    set_error("pcg workspace too small");
+    return HF_ERR_WORKSPACE;
+  }
+  Ctl c;
+  memset(&c, 0, sizeof(c));
+  c.n = n;
+  c.kp = KP;
+  c.G = grid_for(n, KP);
+  c.tol = 0.0;
+  c.max_iter = 1 << 30;
+  c.normb = L.normb; c.rz = L.rz; c.alpha = L.alpha; c.beta = L.beta;
+  c.best_res = L.best_res; c.true_res = L.true_res; c.iters = L.iters;
+  c.best_iter = L.best_iter; c.state = L.state; c.xmask = L.xmask; c.pmask = L.pmask;
+  c.freeze = nullptr; c.part0 = L.part0; c.part1 = L.part1; c.counter = L.counter;
+  c.summary = L.summary;
+  Csr csr{A->indptr, A->indices, A->val};
+  HF_CUDA(cudaMemsetAsync(L.counter, 0, sizeof(unsigned int) * 4, stream));
+  k_init<KP><<<c.G, BLOCK, 0, stream>>>(c, B, d, X, L.R, L.P);
+  HF_LAUNCH_CHECK();
+  count_launches(1 + 3L * rounds);
+  cudaEvent_t ev[4];
+  for (auto& e : ev) HF_CUDA(cudaEventCreate(&e));
+  double acc[3] = {0, 0, 0};
+  for (int r = 0; r < rounds; ++r) {
+    cudaEventRecord(ev[0], stream);
+    k_spmm_pq<KP><<<c.G, BLOCK, 0, stream>>>(c, csr, L.P, L.Q);
+    cudaEventRecord(ev[1], stream);
+    k_update_r<KP><<<c.G, BLOCK, 0, stream>>>(c, L.Q, L.R, d);
+    cudaEventRecord(ev[2], stream);
+    k_update_xp<KP><<<c.G, BLOCK, 0, stream>>>(c, SUM_MASKED, X, L.P, L.R, d);
+    cudaEventRecord(ev[3], stream);
+    HF_CUDA(cudaEventSynchronize(ev[3]));
+    for (int k = 0; k < 3; ++k) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, ev[k], ev[k + 1]);
+      acc[k] += t;
+    }
+  }
+  for (auto& e : ev) cudaEventDestroy(e);
+  HF_LAUNCH_CHECK();
+  for (int k = 0; k < 3; ++k) ms3[k] = (float)(acc[k] / (rounds > 0 ? rounds : 1));
   return HF_OK;
 }
 
@@ -879,6 +932,28 @@ extern "C" int hf_pcg_multi(const hf_csr* A, const double* d, const double* B, i
 #undef HF_PCG_CASE
 }
 
+extern "C" int hf_pcg_profile(const hf_csr* A, const double* d, const double* B, int32_t n,
+                              int32_t kp, int32_t rounds, double* X, float* ms3, void* ws,
+                              size_t ws_bytes, void* stream) {
+  if (!A || !d || !B || !X || !ms3 || !ws || n <= 0 || rounds < 1) {
+    set_error("hf_pcg_profile: bad argument");
+    return HF_ERR_ARG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  switch (kp) {
+    case 2: return pcg::profile<2>(A, d, B, n, rounds, X, ms3, ws, ws_bytes, s);
+    case 4: return pcg::profile<4>(A, d, B, n, rounds, X, ms3, ws, ws_bytes, s);
+    case 8: return pcg::profile<8>(A, d, B, n, rounds, X, ms3, ws, ws_bytes, s);
+    case 16: return pcg::profile<16>(A, d, B, n, rounds, X, ms3, ws, ws_bytes, s);
+    case 32: return pcg::profile<32>(A, d, B, n, rounds, X, ms3, ws, ws_bytes, s);
+    case 64: return pcg::profile<64>(A, d, B, n, rounds, X, ms3, ws, ws_bytes, s);
+    case 128: return pcg::profile<128>(A, d, B, n, rounds, X, ms3, ws, ws_bytes, s);
+    default:
+      set_error("hf_pcg_profile: unsupported kp=%d", kp);
+      return HF_ERR_ARG;
+  }
+}
+
 extern "C" int hf_ldp(const hf_csr* A, double* d, int32_t* zero_count, int32_t* n_zero_rows,
                       void* stream) {
   if (!A || !d || !zero_count || !n_zero_rows) {
@@ -889,6 +964,7 @@ extern "C" int hf_ldp(const hf_csr* A, double* d, int32_t* zero_count, int32_t* 
   HF_CUDA(cudaMemsetAsync(zero_count, 0, sizeof(int32_t), s));
   const int n = A->n_rows;
   if (n > 0) pcg::k_ldp<<<(n + 255) / 256, 256, 0, s>>>(n, A->indptr, A->val, d, zero_count);
+  count_launches(1);
   HF_LAUNCH_CHECK();
   int hz = 0;
   HF_CUDA(cudaMemcpyAsync(&hz, zero_count, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -915,6 +991,7 @@ static int prune_scan(const hf_csr* A, void* ws, size_t ws_bytes, int32_t** off_
   int32_t* scratch = cv.take<int32_t>(scan_scratch_elems(n));
   int32_t* tot = cv.take<int32_t>(4);
   pcg::k_prune_count<<<(n + 255) / 256, 256, 0, s>>>(n, A->indptr, A->val, cnt);
+  count_launches(1);
   HF_LAUNCH_CHECK();
   int rc = exclusive_scan_i32(cnt, off, n, scratch, tot, s);
   if (rc) return rc;
@@ -952,6 +1029,7 @@ extern "C" int hf_csr_prune_fill(const hf_csr* A, void* ws, size_t ws_bytes, int
   const int n = A->n_rows;
   pcg::k_prune_fill<<<(n + 256) / 256, 256, 0, s>>>(n, A->indptr, A->indices, A->val, off,
                                                      indptr_out, indices_out, val_out, total);
+  count_launches(1);
   HF_LAUNCH_CHECK();
   return HF_OK;
 }

@@ -1,6 +1,6 @@
 // Post-solve lead-field kernels for sm_100a (leadfield.py:104-237).
 //
-//   k_bt_t / k_sym   M = C - B'T, M = (M + M')/2           (leadfield.py:107-108)
+//   k_bt_t           raw response block C - B'T[:, cols]       (leadfield.py:107)
 //   k_lf_tile        LF tile = W (G'T)'_tile  — the (G'T)' tile is gathered
 //                    from T rows into shared memory (<= 8 nonzeros per source
 //                    column), then multiplied by W = -R M^-1 on the fp64 tensor
@@ -12,22 +12,17 @@ namespace hf {
 namespace tail {
 
 // ---------------------------------------------------------------- response
-__global__ void k_bt_t(int L, const int32_t* __restrict__ ptr, const int32_t* __restrict__ idx,
-                       const double* __restrict__ val, const double* __restrict__ T, int ldt,
-                       const double* __restrict__ Cdiag, double* __restrict__ Mraw) {
+__global__ void k_bt_t(int L, int col0, int ncols, const int32_t* __restrict__ ptr,
+                       const int32_t* __restrict__ idx, const double* __restrict__ val,
+                       const double* __restrict__ T, int ldt, const double* __restrict__ Cdiag,
+                       double* __restrict__ Mraw) {
   const int l = blockIdx.x;
-  for (int c = threadIdx.x; c < L; c += blockDim.x) {
+  for (int c = threadIdx.x; c < ncols; c += blockDim.x) {
     double acc = 0.0;  // (B'T)[l, c], ascending node order as csc_matvecs
     for (int q = ptr[l]; q < ptr[l + 1]; ++q) acc += val[q] * T[(size_t)idx[q] * ldt + c];
-    const double cl = (l == c) ? Cdiag[l] : 0.0;
-    Mraw[(size_t)l * L + c] = cl - acc;
+    const double cl = (l == col0 + c) ? Cdiag[l] : 0.0;
+    Mraw[(size_t)l * ncols + c] = cl - acc;
   }
-}
-
-__global__ void k_sym(int L, const double* __restrict__ Mraw, double* __restrict__ M) {
-  const int l = blockIdx.x;
-  for (int c = threadIdx.x; c < L; c += blockDim.x)
-    M[(size_t)l * L + c] = 0.5 * (Mraw[(size_t)l * L + c] + Mraw[(size_t)c * L + l]);
 }
 
 // ---------------------------------------------------------------- DMMA tile GEMM
@@ -47,41 +42,41 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
 // Output out[l * ldo + c] for l < L, c < ncols.
 template <int MODE>
 __global__ void __launch_bounds__(LF_THREADS)
-    k_lf_tile(int L, int Lp, int ncols, const double* __restrict__ T, int ldt,
+    k_lf_tile(int L, int K, int Kp, int ncols, const double* __restrict__ T, int ldt,
               const int32_t* __restrict__ gptr, const int32_t* __restrict__ gidx,
               const double* __restrict__ gval, const double* __restrict__ Qc,
-              const double* __restrict__ W, double* __restrict__ out, int ldo) {
-  extern __shared__ double sB[];  // [Lp][LF_SBS]
+              const double* __restrict__ W, int ldw, double* __restrict__ out, int ldo) {
+  extern __shared__ double sB[];  // [Kp][LF_SBS]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c0 = blockIdx.x * LF_NC;
   // phase 1: B tile
-  for (int o = tid; o < Lp * LF_NC; o += LF_THREADS) {
-    const int k = o % Lp, cc = o / Lp, c = c0 + cc;
+  for (int o = tid; o < Kp * LF_NC; o += LF_THREADS) {
+    const int k = o % Kp, cc = o / Kp, c = c0 + cc;
     double acc = 0.0;
-    if (k < L && c < ncols) {
+    if (k < K && c < ncols) {
       if (MODE == 0) {
         for (int q = gptr[c]; q < gptr[c + 1]; ++q)
           acc += __ldg(gval + q) * __ldg(T + (size_t)__ldg(gidx + q) * ldt + k);
       } else {
-        acc = __ldg(Qc + (size_t)c * L + k);
+        acc = __ldg(Qc + (size_t)c * K + k);
       }
     }
     sB[k * LF_SBS + cc] = acc;
   }
   __syncthreads();
-  // phase 2: out tile (Lp x LF_NC) = W (Lp x Lp) * sB; warp owns row blocks
-  // rb = warp, warp+8, ... and all LF_NC/8 column blocks.
+  // phase 2: out tile (L x LF_NC) = W (L x K) * sB (K x LF_NC); warp owns row
+  // blocks rb = warp, warp+8, ... and all LF_NC/8 column blocks.
   const int g = lane >> 2, t4 = lane & 3;
-  const int nrb = Lp / 8;
+  const int nrb = (L + 7) / 8;
   for (int rb = warp; rb < nrb; rb += LF_THREADS / 32) {
     double d[LF_NC / 8][2];
 #pragma unroll
     for (int j = 0; j < LF_NC / 8; ++j) d[j][0] = d[j][1] = 0.0;
     const int row = rb * 8 + g;
-    const double* wrow = W + (size_t)row * L;
-    for (int k0 = 0; k0 < Lp; k0 += 4) {
+    const double* wrow = W + (size_t)row * ldw;
+    for (int k0 = 0; k0 < Kp; k0 += 4) {
       const int kk = k0 + t4;
-      const double a = (row < L && kk < L) ? __ldg(wrow + kk) : 0.0;
+      const double a = (row < L && kk < K) ? __ldg(wrow + kk) : 0.0;
 #pragma unroll
       for (int j = 0; j < LF_NC / 8; ++j) {
         const double b = sB[kk * LF_SBS + j * 8 + g];
@@ -216,52 +211,58 @@ __global__ void __launch_bounds__(ES_THREADS)
 using namespace hf;
 
 extern "C" int hf_response_matrix(const hf_csr* Bt, const double* T, int32_t ldt, int32_t L,
-                                  const double* Cdiag, double* M, double* ws, void* stream) {
-  if (!Bt || !T || !Cdiag || !M || !ws || L <= 0 || Bt->n_rows != L || ldt < L) {
+                                  int32_t col0, int32_t ncols, const double* Cdiag, double* Mraw,
+                                  void* stream) {
+  if (!Bt || !T || !Cdiag || !Mraw || L <= 0 || Bt->n_rows != L || ncols < 0 || ldt < ncols ||
+      col0 < 0 || col0 + ncols > L) {
     set_error("hf_response_matrix: bad argument");
     return HF_ERR_ARG;
   }
+  if (ncols == 0) return HF_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const int th = L < 256 ? ((L + 31) / 32) * 32 : 256;
-  tail::k_bt_t<<<L, th, 0, s>>>(L, Bt->indptr, Bt->indices, Bt->val, T, ldt, Cdiag, ws);
-  tail::k_sym<<<L, th, 0, s>>>(L, ws, M);
+  const int th = ncols < 256 ? ((ncols + 31) / 32) * 32 : 256;
+  tail::k_bt_t<<<L, th, 0, s>>>(L, col0, ncols, Bt->indptr, Bt->indices, Bt->val, T, ldt, Cdiag,
+                                Mraw);
   HF_LAUNCH_CHECK();
+  count_launches(1);
   return HF_OK;
 }
 
-static int lf_launch(int mode, const double* T, int ldt, int L, const hf_csr* Gt, const double* Qc,
-                     int ncols, const double* W, double* out, int ldo, cudaStream_t s) {
-  if (L <= 0 || L > 1024 || ncols < 0) {
-    set_error("lead-field tail: unsupported L=%d", L);
+static int lf_launch(int mode, const double* T, int ldt, int L, int K, const hf_csr* Gt,
+                     const double* Qc, int ncols, const double* W, int ldw, double* out, int ldo,
+                     cudaStream_t s) {
+  if (L <= 0 || K <= 0 || K > 1024 || ncols < 0 || ldw < K) {
+    set_error("lead-field tail: unsupported L=%d K=%d", L, K);
     return HF_ERR_ARG;
   }
   if (ncols == 0) return HF_OK;
-  const int Lp = ((L + 7) / 8) * 8;
-  const size_t smem = sizeof(double) * Lp * tail::LF_SBS;
+  count_launches(1);
+  const int Kp = ((K + 7) / 8) * 8;
+  const size_t smem = sizeof(double) * Kp * tail::LF_SBS;
   const int grid = (ncols + tail::LF_NC - 1) / tail::LF_NC;
   if (mode == 0) {
     HF_CUDA(cudaFuncSetAttribute(tail::k_lf_tile<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-    tail::k_lf_tile<0><<<grid, tail::LF_THREADS, smem, s>>>(L, Lp, ncols, T, ldt, Gt->indptr,
-                                                            Gt->indices, Gt->val, nullptr, W, out,
-                                                            ldo);
+    tail::k_lf_tile<0><<<grid, tail::LF_THREADS, smem, s>>>(L, K, Kp, ncols, T, ldt, Gt->indptr,
+                                                            Gt->indices, Gt->val, nullptr, W, ldw,
+                                                            out, ldo);
   } else {
     HF_CUDA(cudaFuncSetAttribute(tail::k_lf_tile<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem));
-    tail::k_lf_tile<1><<<grid, tail::LF_THREADS, smem, s>>>(L, Lp, ncols, nullptr, 0, nullptr,
-                                                            nullptr, nullptr, Qc, W, out, ldo);
+    tail::k_lf_tile<1><<<grid, tail::LF_THREADS, smem, s>>>(L, K, Kp, ncols, nullptr, 0, nullptr,
+                                                            nullptr, nullptr, Qc, W, ldw, out, ldo);
   }
   HF_LAUNCH_CHECK();
   return HF_OK;
 }
 
-extern "C" int hf_lf_tail(const double* T, int32_t ldt, int32_t L, const hf_csr* Gt,
-                          const double* W, double* LF, void* stream) {
-  if (!T || !Gt || !W || !LF || ldt < L) {
+extern "C" int hf_lf_tail(const double* T, int32_t ldt, int32_t K, const hf_csr* Gt,
+                          const double* W, int32_t L, int32_t ldw, double* LF, void* stream) {
+  if (!T || !Gt || !W || !LF || ldt < K) {
     set_error("hf_lf_tail: bad argument");
     return HF_ERR_ARG;
   }
-  return lf_launch(0, T, ldt, L, Gt, nullptr, Gt->n_rows, W, LF, Gt->n_rows,
+  return lf_launch(0, T, ldt, L, K, Gt, nullptr, Gt->n_rows, W, ldw, LF, Gt->n_rows,
                    reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -271,7 +272,7 @@ extern "C" int hf_dense_lf(const double* Qc, int32_t ncols, int32_t L, const dou
     set_error("hf_dense_lf: bad argument");
     return HF_ERR_ARG;
   }
-  return lf_launch(1, nullptr, 0, L, nullptr, Qc, ncols, W, out, ldo,
+  return lf_launch(1, nullptr, 0, L, L, nullptr, Qc, ncols, W, L, out, ldo,
                    reinterpret_cast<cudaStream_t>(stream));
 }
 
@@ -299,5 +300,6 @@ extern "C" int hf_eit_sens(const double* nodes, const int32_t* tetra, const int3
   tail::k_eit_sens<<<grid, tail::ES_THREADS, smem, s>>>(nodes, tetra, dof_elems, dof_ptr, n_dofs,
                                                         ground, T, ldt, L, U, ldu, P, Q);
   HF_LAUNCH_CHECK();
+  count_launches(1);
   return HF_OK;
 }

@@ -1,0 +1,114 @@
+"""Device-resident EEG lead-field build (the BASELINE.json hot path end to end).
+
+`EegEngine` stages one problem in HBM once — mesh (nodes, int32 tetra,
+sigma), electrode contact triangles, the RHS block of this rank's electrode
+columns, B' and G' as CSR — and then every `build()` runs the whole path
+without host round trips of n-sized data:
+
+  hf_p1_blocks + hf_p1_assemble_*   A (fem.py:197-224)
+  hf_ldp, hf_csr_prune_*            preconditioner, zero-free SpMM copy
+  hf_pcg_multi                      T[:, block] = A^-1 B[:, block] (solver.py:114-141)
+  hf_response_matrix                (C - B'T)[:, block]            (leadfield.py:107)
+  host (L x L)                      M = (M + M')/2, W = -R M^-1    (leadfield.py:108-119)
+  hf_lf_tail                        LF (partial over the block) = W[:, block] (G'T_block)'
+
+With one rank the block is every electrode.  `distributed.eeg_leadfield_sharded`
+splits the electrode columns over ranks and exchanges the two small results
+(M blocks, LF partial sums) with NCCL.
+"""
+from __future__ import annotations
+
+import numpy as np
+import scipy.sparse as sp
+import torch
+
+from . import model
+from .device import DeviceCsr, PcgOperator, device
+from .fem import DeviceMesh, assemble_device, blocks_device
+from .leadfield import lf_tail_device, response_block_device, response_operator, symmetrize
+from .solver import PcgConfig, _raise_failed, rhs_block, solve_block
+
+
+def column_blocks(L, world):
+    """Contiguous electrode blocks, sizes differing by at most one."""
+    base, extra = divmod(L, world)
+    out, c = [], 0
+    for r in range(world):
+        k = base + (1 if r < extra else 0)
+        out.append((c, c + k))
+        c += k
+    return out
+
+
+class EegEngine:
+    """One rank's share of an EEG lead-field build with inputs resident in HBM."""
+
+    def __init__(self, mesh, electrodes, G, cfg=PcgConfig(), B=None, C=None, R=None,
+                 columns=None, dev=None):
+        dev = dev or device()
+        self.cfg = cfg
+        self.h2d_bytes = 0
+        self.dmesh = DeviceMesh(mesh.nodes, mesh.tetra, dev)
+        self.h2d_bytes += self.dmesh.nodes.numel() * 8 + self.dmesh.tetra.numel() * 4
+        sig = np.asarray(mesh.sigma, dtype=np.float64)
+        self.sigma = torch.from_numpy(np.ascontiguousarray(sig)).to(dev)
+        self.h2d_bytes += sig.nbytes
+        if B is None or C is None or R is None:
+            B, C, R = model.assemble_B_C_R(mesh, electrodes)
+        self.L = B.shape[1]
+        self.n = mesh.n_nodes if hasattr(mesh, "n_nodes") else len(mesh.nodes)
+        self.ground = model.ground_node(mesh, electrodes)
+        tri, coef = model.electrode_contacts(electrodes)
+        self.etri = torch.from_numpy(np.ascontiguousarray(tri, dtype=np.int32)).to(dev)
+        self.ecoef = torch.from_numpy(np.ascontiguousarray(coef, dtype=np.float64)).to(dev)
+        self.h2d_bytes += tri.size * 4 + coef.nbytes
+        self.c0, self.c1 = columns if columns is not None else (0, self.L)
+        Bc = sp.csc_matrix(B)[:, self.c0:self.c1]
+        self.Bd = rhs_block(Bc, dev=dev)
+        self.Bt = DeviceCsr.from_scipy(sp.csr_matrix(sp.csr_matrix(B).T), dev)
+        self.Cdiag = torch.from_numpy(np.ascontiguousarray(C.diagonal(), dtype=np.float64)).to(dev)
+        self.R = np.asarray(R, dtype=np.float64)
+        Gs = G if sp.issparse(G) else sp.csr_matrix(np.asarray(G, dtype=float))
+        self.Gt = DeviceCsr.from_scipy(sp.csr_matrix(Gs.T), dev)
+        self.ncols = Gs.shape[1]
+        self.h2d_bytes += (Bc.nnz * 20 + self.Bt.nnz * 12 + self.Gt.nnz * 12 + 8 * self.L
+                           + 4 * (self.n + 1) + 4 * (self.ncols + 1) + 4 * (self.L + 1))
+        self.last_info = None
+
+    # ---- stages -------------------------------------------------------------
+    def assemble(self):
+        blocks = blocks_device(self.dmesh, self.sigma, 0.0)
+        return assemble_device(self.dmesh, blocks, self.n, self.etri, self.ecoef, self.ground)
+
+    def solve(self, A):
+        op = PcgOperator(A, self.cfg.preconditioner)
+        if op.n_zero_rows:
+            from .errors import SingularPreconditionerError
+            raise SingularPreconditionerError(f"{op.n_zero_rows} zero row(s) in the operator")
+        T, info = solve_block(op, self.Bd, self.cfg)
+        _raise_failed(info, T, self.cfg, column_tag=True)
+        self.last_info = info
+        return T
+
+    def response_block(self, T):
+        return response_block_device(self.Bt, T, self.L, self.Cdiag, self.c0)
+
+    def lf_partial(self, T, W):
+        return lf_tail_device(T, self.Gt, np.ascontiguousarray(W[:, self.c0:self.c1]))
+
+    # ---- single-rank build --------------------------------------------------
+    def build(self, to_host=False):
+        """Whole LF build on this device (requires every column: columns=(0, L))."""
+        if (self.c0, self.c1) != (0, self.L):
+            raise ValueError("build() needs all electrode columns; use distributed.eeg_leadfield_sharded")
+        A = self.assemble()
+        T = self.solve(A)
+        M = symmetrize(self.response_block(T).cpu().numpy())
+        W = response_operator(M, self.R)
+        LF = self.lf_partial(T, W)
+        return LF.cpu().numpy() if to_host else LF
+
+
+def eeg_leadfield_from_mesh(mesh, electrodes, G, cfg=PcgConfig()):
+    """Host mesh/electrodes/G in, host lead field (L x ncols) out — the e2e call."""
+    return EegEngine(mesh, electrodes, G, cfg).build(to_host=True)

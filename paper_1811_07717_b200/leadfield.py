@@ -115,16 +115,25 @@ class DeviceSystem:
         self.Cdiag = torch.from_numpy(np.ascontiguousarray(sys.C.diagonal(), dtype=np.float64)).to(dev)
 
 
+def response_block_device(Bt, T, L, Cdiag, col0=0):
+    """Raw response block (C - B'T)[:, col0:col0+k] (device L x k) for the k
+    transfer columns held in T (leadfield.py:107)."""
+    k = T.shape[1]
+    Mraw = torch.empty((L, k), dtype=torch.float64, device=T.device)
+    N.check("hf_response_matrix", N.lib.hf_response_matrix(
+        N.C.byref(Bt.struct), N.ptr(T), T.stride(0), L, int(col0), k, N.ptr(Cdiag), N.ptr(Mraw),
+        N.stream_handle()))
+    return Mraw
+
+
+def symmetrize(Mraw):
+    """M = (M + M')/2, the exact-symmetry step of leadfield.py:108."""
+    return 0.5 * (Mraw + Mraw.T)
+
+
 def response_matrix_device(dsys, T):
     """M = C - B'T, symmetrised (leadfield.py:107-108), as a host array."""
-    L = dsys.L
-    dev = T.device
-    M = torch.empty((L, L), dtype=torch.float64, device=dev)
-    ws = torch.empty((L, L), dtype=torch.float64, device=dev)
-    N.check("hf_response_matrix", N.lib.hf_response_matrix(
-        N.C.byref(dsys.Bt.struct), N.ptr(T), T.stride(0), L, N.ptr(dsys.Cdiag), N.ptr(M),
-        N.ptr(ws), N.stream_handle()))
-    return M.cpu().numpy()
+    return symmetrize(response_block_device(dsys.Bt, T, dsys.L, dsys.Cdiag).cpu().numpy())
 
 
 def _solve_response(M, rhs):
@@ -151,14 +160,20 @@ def electrode_response(sys, cfg=PcgConfig(), threads=1):
     return np.ascontiguousarray(T.cpu().numpy()), M
 
 
-def lf_tail_device(T, L, Gt, W):
-    """LF (L x ncols, device) = W (G'T)' by hf_lf_tail."""
+def lf_tail_device(T, Gt, W):
+    """LF (L x ncols, device) = W (G'T)' by hf_lf_tail; T holds K columns and W
+    is L x K (the whole response operator, or one rank's column block of it)."""
     dev = T.device
+    K = T.shape[1]
+    Wh = np.ascontiguousarray(W, dtype=np.float64)
+    L = Wh.shape[0]
+    if Wh.shape[1] != K:
+        raise ValueError(f"W has {Wh.shape[1]} columns, T has {K}")
     ncols = Gt.shape[0]
     LF = torch.empty((L, ncols), dtype=torch.float64, device=dev)
-    Wd = torch.from_numpy(np.ascontiguousarray(W, dtype=np.float64)).to(dev)
-    N.check("hf_lf_tail", N.lib.hf_lf_tail(N.ptr(T), T.stride(0), L, N.C.byref(Gt.struct),
-                                           N.ptr(Wd), N.ptr(LF), N.stream_handle()))
+    Wd = torch.from_numpy(Wh).to(dev)
+    N.check("hf_lf_tail", N.lib.hf_lf_tail(N.ptr(T), T.stride(0), K, N.C.byref(Gt.struct),
+                                           N.ptr(Wd), L, K, N.ptr(LF), N.stream_handle()))
     return LF
 
 
@@ -176,7 +191,7 @@ def eeg_leadfield(sys, cfg=PcgConfig(), threads=1):
     W = response_operator(M, sys.R)
     G = sys.G if sp.issparse(sys.G) else sp.csr_matrix(np.asarray(sys.G, dtype=float))
     Gt = DeviceCsr.from_scipy(sp.csr_matrix(G.T), T.device)
-    LF = lf_tail_device(T, dsys.L, Gt, W).cpu().numpy()
+    LF = lf_tail_device(T, Gt, W).cpu().numpy()
     src = sys.source_space
     return LeadField(matrix=LF, positions=src.positions if src is not None else None,
                      orientations=src.orientations if src is not None else None, modality="eeg")
@@ -260,4 +275,5 @@ def eit_leadfield(sys, dofs, currents, cfg=PcgConfig(), threads=1):
 
 __all__ = ["LeadField", "EitDofMap", "build_dof_map", "electrode_response", "eeg_leadfield",
            "check_current_patterns", "adjacent_pair_patterns", "eit_forward", "eit_leadfield",
-           "DeviceSystem", "lf_tail_device", "response_operator"]
+           "DeviceSystem", "lf_tail_device", "response_operator", "response_block_device",
+           "symmetrize"]
