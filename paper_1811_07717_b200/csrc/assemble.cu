@@ -22,10 +22,24 @@ constexpr int ROW_WARPS = 8;          // warps per block in the row kernels
 constexpr int MAX_INC = 128;          // incident elements per node supported
 constexpr int MAX_CAND = 4 * MAX_INC; // candidate columns per row
 
+// Element arithmetic uses explicitly rounded operations (no FMA contraction):
+// mirrored Kuhn tetrahedra then produce bitwise-opposite off-diagonal
+// contributions, which cancel to exact zeros in the row sums — the explicit
+// zeros of the reference's pattern (fem.py:96-102) — instead of 1e-20 residue
+// that the SpMM would have to stream.
+#define MUL(a, b) __dmul_rn((a), (b))
+#define ADD(a, b) __dadd_rn((a), (b))
+#define SUB(a, b) __dsub_rn((a), (b))
+
 __device__ __forceinline__ double det3(const double a[3][3]) {
-  return a[0][0] * (a[1][1] * a[2][2] - a[1][2] * a[2][1]) -
-         a[0][1] * (a[1][0] * a[2][2] - a[1][2] * a[2][0]) +
-         a[0][2] * (a[1][0] * a[2][1] - a[1][1] * a[2][0]);
+  const double c0 = SUB(MUL(a[1][1], a[2][2]), MUL(a[1][2], a[2][1]));
+  const double c1 = SUB(MUL(a[1][0], a[2][2]), MUL(a[1][2], a[2][0]));
+  const double c2 = SUB(MUL(a[1][0], a[2][1]), MUL(a[1][1], a[2][0]));
+  return ADD(SUB(MUL(a[0][0], c0), MUL(a[0][1], c1)), MUL(a[0][2], c2));
+}
+
+__device__ __forceinline__ double dot3(const double* a, const double* b) {
+  return ADD(ADD(MUL(a[0], b[0]), MUL(a[1], b[1])), MUL(a[2], b[2]));
 }
 
 // vol, grads (4x3) of element with vertex coordinates p[4][3]  (fem.py:31-41)
@@ -34,22 +48,21 @@ __device__ __forceinline__ double p1_gradients(const double p[4][3], double g[4]
 #pragma unroll
   for (int r = 0; r < 3; ++r)
 #pragma unroll
-    for (int k = 0; k < 3; ++k) J[r][k] = p[k + 1][r] - p[0][r];
+    for (int k = 0; k < 3; ++k) J[r][k] = SUB(p[k + 1][r], p[0][r]);
   const double det = det3(J);
-  const double inv_det = 1.0 / det;
   // inverse = adj(J)/det; row k of the inverse is grad(lambda_{k+1})
-  g[1][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) * inv_det;
-  g[1][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * inv_det;
-  g[1][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * inv_det;
-  g[2][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) * inv_det;
-  g[2][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * inv_det;
-  g[2][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * inv_det;
-  g[3][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) * inv_det;
-  g[3][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * inv_det;
-  g[3][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * inv_det;
+  g[1][0] = __ddiv_rn(SUB(MUL(J[1][1], J[2][2]), MUL(J[1][2], J[2][1])), det);
+  g[1][1] = __ddiv_rn(SUB(MUL(J[0][2], J[2][1]), MUL(J[0][1], J[2][2])), det);
+  g[1][2] = __ddiv_rn(SUB(MUL(J[0][1], J[1][2]), MUL(J[0][2], J[1][1])), det);
+  g[2][0] = __ddiv_rn(SUB(MUL(J[1][2], J[2][0]), MUL(J[1][0], J[2][2])), det);
+  g[2][1] = __ddiv_rn(SUB(MUL(J[0][0], J[2][2]), MUL(J[0][2], J[2][0])), det);
+  g[2][2] = __ddiv_rn(SUB(MUL(J[0][2], J[1][0]), MUL(J[0][0], J[1][2])), det);
+  g[3][0] = __ddiv_rn(SUB(MUL(J[1][0], J[2][1]), MUL(J[1][1], J[2][0])), det);
+  g[3][1] = __ddiv_rn(SUB(MUL(J[0][1], J[2][0]), MUL(J[0][0], J[2][1])), det);
+  g[3][2] = __ddiv_rn(SUB(MUL(J[0][0], J[1][1]), MUL(J[0][1], J[1][0])), det);
 #pragma unroll
-  for (int k = 0; k < 3; ++k) g[0][k] = -(g[1][k] + g[2][k] + g[3][k]);
-  return det / 6.0;
+  for (int k = 0; k < 3; ++k) g[0][k] = -ADD(ADD(g[1][k], g[2][k]), g[3][k]);
+  return __ddiv_rn(det, 6.0);
 }
 
 __device__ __forceinline__ void load_element(const double* __restrict__ nodes,
@@ -82,18 +95,18 @@ __global__ void k_blocks(const double* __restrict__ nodes, const int32_t* __rest
   if (sigma_cols == 6) {
     const double* s = sigma + 6 * (size_t)t;  // sigma rows align with the subset
     const double S[3][3] = {{s[0], s[3], s[4]}, {s[3], s[1], s[5]}, {s[4], s[5], s[2]}};
-    const double d1 = S[0][0], d2 = S[0][0] * S[1][1] - S[0][1] * S[0][1], d3 = det3(S);
+    const double d1 = S[0][0], d2 = SUB(MUL(S[0][0], S[1][1]), MUL(S[0][1], S[0][1])), d3 = det3(S);
     if (d1 <= 0.0 || d2 <= 0.0 || d3 <= 0.0) fl |= 4;  // Sylvester, fem.py:62-67
     double Sg[4][3];
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) Sg[j][k] = S[k][0] * g[j][0] + S[k][1] * g[j][1] + S[k][2] * g[j][2];
+      for (int k = 0; k < 3; ++k) Sg[j][k] = dot3(S[k], g[j]);
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        out[4 * i + j] = (g[i][0] * Sg[j][0] + g[i][1] * Sg[j][1] + g[i][2] * Sg[j][2]) * vol;
+        out[4 * i + j] = MUL(dot3(g[i], Sg[j]), vol);
   } else {
     double sg;
     if (sigma_cols == 1) {
@@ -102,12 +115,12 @@ __global__ void k_blocks(const double* __restrict__ nodes, const int32_t* __rest
     } else {
       sg = sigma_scalar;
     }
-    const double w = vol * sg;
+    const double w = MUL(vol, sg);
 #pragma unroll
     for (int i = 0; i < 4; ++i)
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-        out[4 * i + j] = (g[i][0] * g[j][0] + g[i][1] * g[j][1] + g[i][2] * g[j][2]) * w;
+        out[4 * i + j] = MUL(dot3(g[i], g[j]), w);
   }
   if (fl) atomicOr(flags, fl);
 }
@@ -264,7 +277,7 @@ __global__ void __launch_bounds__(ROW_WARPS * 32)
       const int32_t* tt = etri + 3 * (size_t)t;
 #pragma unroll
       for (int lb = 0; lb < 3; ++lb)
-        if (tt[lb] == col) acc += ecoef[t] * ((la == lb ? 2.0 : 1.0) / 12.0);
+        if (tt[lb] == col) acc += MUL(ecoef[t], (la == lb ? 2.0 : 1.0) / 12.0);
     }
     indices[base + p] = col;
     val[base + p] = acc;

@@ -77,9 +77,16 @@ struct Map {
   static constexpr int RB = BLOCK / LPR;                    // rows per block pass
   static constexpr int SPLIT = BLOCK / KP;                  // last-block reduction splits
   static constexpr int RED = (NWARP * KP > BLOCK) ? NWARP * KP : BLOCK;
+  // row tiles in flight per thread in the streaming kernels (register budget: 64)
+  static constexpr int UR = 2;                                    // k_update_r
+  static constexpr int UX = (CPL == 4) ? 1 : 2;                   // k_update_xp
 };
 
-__host__ __device__ inline int rows_per_block(int n, int G) { return (n + G - 1) / G; }
+// Rows are dealt to blocks in tiles of RB rows, round-robin (tile t -> block
+// t % G): the whole grid sweeps the mesh as one narrow band, so the rows a
+// gather touches one z-plane up or down are still in L2 (a contiguous chunk
+// per block made every block's neighbours far apart in time: 4x DRAM re-reads).
+__host__ __device__ inline int n_tiles(int n, int rb) { return (n + rb - 1) / rb; }
 
 template <int CPL>
 __device__ __forceinline__ void ld_cols(const double* __restrict__ p, double (&v)[CPL]) {
@@ -200,12 +207,13 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
   __shared__ double sm[2 * M::RED];
   __shared__ double tot[2 * KP];
   const int tid = threadIdx.x, gl = tid / M::LPR, glane = tid % M::LPR;
-  const int rpb = rows_per_block(c.n, c.G);
-  const int r0 = blockIdx.x * rpb, r1 = min(c.n, r0 + rpb);
+  const int nt = n_tiles(c.n, M::RB);
   double v[2][M::CPL];
 #pragma unroll
   for (int k = 0; k < M::CPL; ++k) v[0][k] = v[1][k] = 0.0;
-  for (int row = r0 + gl; row < r1; row += M::RB) {
+  for (int t = blockIdx.x; t < nt; t += c.G) {
+    const int row = t * M::RB + gl;
+    if (row >= c.n) continue;
     const size_t o = (size_t)row * KP + glane * M::CPL;
     double b[M::CPL], z[M::CPL], zero[M::CPL];
     ld_cols<M::CPL>(B + o, b);
@@ -252,52 +260,244 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
 }
 
 // ---------------------------------------------------------------- SpMM
-// Gathers sum_j a_ij * V[col_j, cols of this lane] for one row; the row's
-// (index, value) pairs are loaded cooperatively by the row group and broadcast
-// with shuffles.  Rows are processed in warp-uniform passes so shuffles never
-// diverge.  `act` masks columns whose value is not needed.
+// The SpMM kernels are latency-bound gathers: they run one 512-thread block
+// per SM with a 128-register budget and keep R rows x GB gathers in flight
+// per lane group (all loads issued before any FMA consumes them).
+#ifndef HF_SPMM_BPS
+#define HF_SPMM_BPS 2
+#endif
+constexpr int SPMM_BLOCKS_PER_SM = HF_SPMM_BPS;
+constexpr int GB = 8;  // gathers per batch
+
 template <int KP>
-__device__ __forceinline__ void row_gather(const Csr& A, const double* __restrict__ V, int row,
-                                           bool valid, bool any, double (&acc)[Map<KP>::CPL]) {
+struct Spmm {
+#ifndef HF_SPMM_R2
+  static constexpr int R = 1;  // rows in flight per row group (pipelined across steps)
+#else
+  static constexpr int R = (Map<KP>::CPL == 4) ? 1 : 2;
+#endif
+};
+
+// acc[r] = sum_j a_ij * V[col_j, lane columns] for the R rows of this row group.
+// The rows' (index, value) pairs are loaded cooperatively by the group and
+// broadcast with shuffles; loop bounds are warp-uniform so shuffles never
+// diverge.  `any` false skips the gathers (no active column in this lane).
+template <int KP, int R>
+__device__ __forceinline__ void gather_rows(const Csr& A, const double* __restrict__ V,
+                                            const int (&row)[R], bool any,
+                                            double (&acc)[R][Map<KP>::CPL]) {
   using M = Map<KP>;
-  const int glane = threadIdx.x % M::LPR;
+  constexpr int CPL = M::CPL, LPR = M::LPR;
+  const int glane = threadIdx.x % LPR;
+  int start[R], len[R];
+  int maxlen = 0;
 #pragma unroll
-  for (int k = 0; k < M::CPL; ++k) acc[k] = 0.0;
-  int start = 0, len = 0;
-  if (valid) {
-    start = A.indptr[row];
-    len = A.indptr[row + 1] - start;
-  }
-  int maxlen = len;
-  if (M::LPR < 32) maxlen = __reduce_max_sync(FULL, (unsigned)len);
-  const double* __restrict__ Vl = V + glane * M::CPL;
-  for (int base = 0; base < maxlen; base += M::LPR) {
-    const int jj = base + glane;
-    int ci = 0;
-    double cv = 0.0;
-    if (jj < len) {
-      ci = __ldg(A.indices + start + jj);
-      cv = __ldg(A.val + start + jj);
+  for (int r = 0; r < R; ++r) {
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) acc[r][k] = 0.0;
+    start[r] = 0;
+    len[r] = 0;
+    if (row[r] >= 0) {
+      start[r] = A.indptr[row[r]];
+      len[r] = A.indptr[row[r] + 1] - start[r];
     }
-    const int nt = min(M::LPR, maxlen - base);
-    if (M::LPR == 1) {
-      if (jj < len && any) {
-        double p[M::CPL];
-        ldg_cols<M::CPL>(Vl + (size_t)ci * KP, p);
+    maxlen = max(maxlen, len[r]);
+  }
+  if (LPR < 32) maxlen = (int)__reduce_max_sync(FULL, (unsigned)maxlen);
+  const double* __restrict__ Vl = V + glane * CPL;
+  for (int c0 = 0; c0 < maxlen; c0 += LPR) {
+    int ci[R];
+    double cv[R];
 #pragma unroll
-        for (int k = 0; k < M::CPL; ++k) acc[k] = fma(cv, p[k], acc[k]);
+    for (int r = 0; r < R; ++r) {
+      const int jj = c0 + glane;
+      ci[r] = 0;
+      cv[r] = 0.0;
+      if (jj < len[r]) {
+        ci[r] = __ldg(A.indices + start[r] + jj);
+        cv[r] = __ldg(A.val + start[r] + jj);
       }
-    } else {
-#pragma unroll 8
-      for (int t = 0; t < nt; ++t) {
-        const int cc = __shfl_sync(FULL, ci, t, M::LPR);
-        const double vv = __shfl_sync(FULL, cv, t, M::LPR);
-        if (base + t < len && any) {
-          double p[M::CPL];
-          ldg_cols<M::CPL>(Vl + (size_t)cc * KP, p);
+    }
+    if (LPR == 1) {  // one row per thread: the thread walks its own entries
 #pragma unroll
-          for (int k = 0; k < M::CPL; ++k) acc[k] = fma(vv, p[k], acc[k]);
+      for (int r = 0; r < R; ++r)
+        if (c0 < len[r] && any) {
+          double g[CPL];
+          ldg_cols<CPL>(Vl + (size_t)ci[r] * KP, g);
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) acc[r][k] = fma(cv[r], g[k], acc[r][k]);
         }
+      continue;
+    }
+    const int nchunk = min(LPR, maxlen - c0);
+    for (int b = 0; b < nchunk; b += GB) {
+      double g[R][GB][CPL];
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int t = 0; t < GB; ++t) {
+          const int e = b + t;
+          const int cc = __shfl_sync(FULL, ci[r], e & (LPR - 1), LPR);
+          if (e < nchunk && c0 + e < len[r] && any) {
+            ldg_cols<CPL>(Vl + (size_t)cc * KP, g[r][t]);
+          } else {
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) g[r][t][k] = 0.0;
+          }
+        }
+#pragma unroll
+      for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int t = 0; t < GB; ++t) {
+          const int e = b + t;
+          const double vv = __shfl_sync(FULL, cv[r], e & (LPR - 1), LPR);
+          if (e < nchunk && c0 + e < len[r]) {
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) acc[r][k] = fma(vv, g[r][t][k], acc[r][k]);
+          }
+        }
+    }
+  }
+}
+
+// Whole-block sweep over this block's rows: calls epi(row[R], acc[R][CPL]).
+// For row groups of >= 16 lanes the CSR stream is software-pipelined in
+// registers: step s gathers with the (index, value) pairs loaded during step
+// s-1 while the pairs of step s+1 and the row pointers of step s+2 are in
+// flight, so a row costs one memory latency instead of three dependent ones
+// (indptr -> indices -> gathered rows).  Lane g of a row group holds the
+// row's entry g; rows with more entries than lanes finish with direct loads.
+template <int KP, int R>
+__device__ __forceinline__ void load_meta(const Ctl& c, const Csr& A, int t0, int nt,
+                                          int (&row)[R], int (&st)[R], int (&ln)[R]) {
+  using M = Map<KP>;
+  const int gl = threadIdx.x / M::LPR;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int t = t0 + r * c.G;
+    const int rw = t * M::RB + gl;
+    row[r] = (t < nt && rw < c.n) ? rw : -1;
+    st[r] = 0;
+    ln[r] = 0;
+    if (row[r] >= 0) {
+      st[r] = __ldg(A.indptr + row[r]);
+      ln[r] = __ldg(A.indptr + row[r] + 1) - st[r];
+    }
+  }
+}
+
+template <int KP, int R>
+__device__ __forceinline__ void load_entries(const Csr& A, const int (&st)[R], const int (&ln)[R],
+                                             int (&ci)[R], double (&cv)[R]) {
+  const int glane = threadIdx.x % Map<KP>::LPR;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    ci[r] = 0;
+    cv[r] = 0.0;
+    if (glane < ln[r]) {
+      ci[r] = __ldg(A.indices + st[r] + glane);
+      cv[r] = __ldg(A.val + st[r] + glane);
+    }
+  }
+}
+
+template <int KP, class Epi>
+__device__ __forceinline__ void spmm_sweep(const Ctl& c, const Csr& A, const double* __restrict__ V,
+                                           bool any, Epi&& epi) {
+  using M = Map<KP>;
+  constexpr int R = Spmm<KP>::R, LPR = M::LPR, CPL = M::CPL;
+  const int nt = n_tiles(c.n, M::RB);
+  const int step = R * c.G;
+  if constexpr (LPR < 16) {
+    const int gl = threadIdx.x / LPR;
+    for (int t0 = blockIdx.x; t0 < nt; t0 += step) {
+      int row[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int t = t0 + r * c.G;
+        row[r] = (t < nt && t * M::RB + gl < c.n) ? t * M::RB + gl : -1;
+      }
+      double acc[R][CPL];
+      gather_rows<KP, R>(A, V, row, any, acc);
+      epi(row, acc);
+    }
+  } else {
+    const int glane = threadIdx.x % LPR;
+    const double* __restrict__ Vl = V + glane * CPL;
+    int row[R], st[R], ln[R], ci[R];
+    double cv[R];
+    int rowN[R], stN[R], lnN[R];
+    int t0 = blockIdx.x;
+    load_meta<KP, R>(c, A, t0, nt, row, st, ln);
+    load_entries<KP, R>(A, st, ln, ci, cv);
+    load_meta<KP, R>(c, A, t0 + step, nt, rowN, stN, lnN);
+    for (; t0 < nt; t0 += step) {
+      int ciN[R], rowNN[R], stNN[R], lnNN[R];
+      double cvN[R];
+      load_entries<KP, R>(A, stN, lnN, ciN, cvN);                 // step s+1 pairs
+      load_meta<KP, R>(c, A, t0 + 2 * step, nt, rowNN, stNN, lnNN);  // step s+2 pointers
+      double acc[R][CPL];
+      int maxlen = 0;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) acc[r][k] = 0.0;
+        maxlen = max(maxlen, ln[r]);
+      }
+      if (LPR < 32) maxlen = (int)__reduce_max_sync(FULL, (unsigned)maxlen);
+      const int inreg = min(maxlen, LPR);
+      for (int b = 0; b < inreg; b += GB) {
+        double g[R][GB][CPL];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int t = 0; t < GB; ++t) {
+            const int e = b + t;
+            const int cc = __shfl_sync(FULL, ci[r], e & (LPR - 1), LPR);
+            if (e < LPR && e < ln[r] && any) {
+              ldg_cols<CPL>(Vl + (size_t)cc * KP, g[r][t]);
+            } else {
+#pragma unroll
+              for (int k = 0; k < CPL; ++k) g[r][t][k] = 0.0;
+            }
+          }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int t = 0; t < GB; ++t) {
+            const int e = b + t;
+            const double vv = __shfl_sync(FULL, cv[r], e & (LPR - 1), LPR);
+            if (e < LPR && e < ln[r]) {
+#pragma unroll
+              for (int k = 0; k < CPL; ++k) acc[r][k] = fma(vv, g[r][t][k], acc[r][k]);
+            }
+          }
+      }
+      if (maxlen > LPR) {  // long rows: remaining entries straight from memory
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+          for (int e = LPR; e < ln[r]; ++e) {
+            const int cc = __ldg(A.indices + st[r] + e);
+            const double vv = __ldg(A.val + st[r] + e);
+            if (any) {
+              double g[CPL];
+              ldg_cols<CPL>(Vl + (size_t)cc * KP, g);
+#pragma unroll
+              for (int k = 0; k < CPL; ++k) acc[r][k] = fma(vv, g[k], acc[r][k]);
+            }
+          }
+      }
+      epi(row, acc);
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        row[r] = rowN[r];
+        st[r] = stN[r];
+        ln[r] = lnN[r];
+        ci[r] = ciN[r];
+        cv[r] = cvN[r];
+        rowN[r] = rowNN[r];
+        stN[r] = stNN[r];
+        lnN[r] = lnNN[r];
       }
     }
   }
@@ -305,9 +505,10 @@ __device__ __forceinline__ void row_gather(const Csr& A, const double* __restric
 
 // q = A p, partial p.q, alpha = rz / p.q       (solver.py:87-88)
 template <int KP>
-__global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
+__global__ void __launch_bounds__(BLOCK, SPMM_BLOCKS_PER_SM)
     k_spmm_pq(Ctl c, Csr A, const double* __restrict__ P, double* __restrict__ Q) {
   using M = Map<KP>;
+  constexpr int R = Spmm<KP>::R;
   __shared__ double sm[M::RED];
   __shared__ double tot[KP];
   __shared__ int s_act[KP];
@@ -322,26 +523,24 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
     act[k] = s_act[glane * M::CPL + k];
     any |= act[k];
   }
-  const int rpb = rows_per_block(c.n, c.G);
-  const int r0 = blockIdx.x * rpb, r1 = min(c.n, r0 + rpb);
+  const int nt = n_tiles(c.n, M::RB);
   double v[1][M::CPL];
 #pragma unroll
   for (int k = 0; k < M::CPL; ++k) v[0][k] = 0.0;
-  for (int base = r0; base < r1; base += M::RB) {
-    const int row = base + gl;
-    const bool valid = row < r1;
-    double acc[M::CPL];
-    row_gather<KP>(A, P, row, valid, any, acc);
-    if (valid && any) {
-      const size_t o = (size_t)row * KP + glane * M::CPL;
-      st_cols<M::CPL>(Q + o, acc);
+  spmm_sweep<KP>(c, A, P, any, [&](const int (&row)[R], double (&acc)[R][M::CPL]) {
+    if (!any) return;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (row[r] < 0) continue;
+      const size_t o = (size_t)row[r] * KP + glane * M::CPL;
+      st_cols<M::CPL>(Q + o, acc[r]);
       double p[M::CPL];
       ldg_cols<M::CPL>(P + o, p);
 #pragma unroll
       for (int k = 0; k < M::CPL; ++k)
-        if (act[k]) v[0][k] += p[k] * acc[k];
+        if (act[k]) v[0][k] += p[k] * acc[r][k];
     }
-  }
+  });
   block_partials<KP, 1>(v, sm, c.part0, nullptr);
   if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
   if (tid < KP) {
@@ -378,27 +577,38 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
     al[k] = s_alpha[glane * M::CPL + k];
     any |= act[k];
   }
-  const int rpb = rows_per_block(c.n, c.G);
-  const int r0 = blockIdx.x * rpb, r1 = min(c.n, r0 + rpb);
+  const int nt = n_tiles(c.n, M::RB);
   double v[2][M::CPL];
 #pragma unroll
   for (int k = 0; k < M::CPL; ++k) v[0][k] = v[1][k] = 0.0;
   if (any) {
-    for (int row = r0 + gl; row < r1; row += M::RB) {
-      const size_t o = (size_t)row * KP + glane * M::CPL;
-      double r[M::CPL], q[M::CPL];
-      ld_cols<M::CPL>(R + o, r);
-      ld_cols<M::CPL>(Q + o, q);
-      const double dd = __ldg(d + row);
+    constexpr int U = M::UR;
+    for (int t0 = blockIdx.x; t0 < nt; t0 += U * c.G) {
+      double r[U][M::CPL], q[U][M::CPL], dd[U];
+      int rows[U];
 #pragma unroll
-      for (int k = 0; k < M::CPL; ++k) {
-        if (act[k]) {
-          r[k] = r[k] - al[k] * q[k];
-          v[0][k] += r[k] * r[k];
-          v[1][k] += r[k] * (r[k] / dd);
+      for (int u = 0; u < U; ++u) {  // all loads first: U rows in flight
+        rows[u] = (t0 + u * c.G < nt) ? (t0 + u * c.G) * M::RB + gl : c.n;
+        if (rows[u] < c.n) {
+          const size_t o = (size_t)rows[u] * KP + glane * M::CPL;
+          ld_cols<M::CPL>(R + o, r[u]);
+          ld_cols<M::CPL>(Q + o, q[u]);
+          dd[u] = __ldg(d + rows[u]);
         }
       }
-      st_cols<M::CPL>(R + o, r);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (rows[u] >= c.n) continue;
+#pragma unroll
+        for (int k = 0; k < M::CPL; ++k) {
+          if (act[k]) {
+            r[u][k] = r[u][k] - al[k] * q[u][k];
+            v[0][k] += r[u][k] * r[u][k];
+            v[1][k] += r[u][k] * (r[u][k] / dd[u]);
+          }
+        }
+        st_cols<M::CPL>(R + (size_t)rows[u] * KP + glane * M::CPL, r[u]);
+      }
     }
   }
   block_partials<KP, 2>(v, sm, c.part0, c.part1);
@@ -471,28 +681,40 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
     anyp |= pm[k];
   }
   if (!anyx && !anyp) return;
-  const int rpb = rows_per_block(c.n, c.G);
-  const int r0 = blockIdx.x * rpb, r1 = min(c.n, r0 + rpb);
-  for (int row = r0 + gl; row < r1; row += M::RB) {
-    const size_t o = (size_t)row * KP + glane * M::CPL;
-    double p[M::CPL];
-    ld_cols<M::CPL>(P + o, p);
-    if (anyx) {
-      double x[M::CPL];
-      ld_cols<M::CPL>(X + o, x);
+  const int nt = n_tiles(c.n, M::RB);
+  constexpr int U = M::UX;
+  for (int t0 = blockIdx.x; t0 < nt; t0 += U * c.G) {
+    double p[U][M::CPL], x[U][M::CPL], r[U][M::CPL], dd[U];
+    int rows[U];
 #pragma unroll
-      for (int k = 0; k < M::CPL; ++k)
-        if (xm[k]) x[k] = x[k] + al[k] * p[k];
-      st_cols<M::CPL>(X + o, x);
+    for (int u = 0; u < U; ++u) {  // all loads first: U rows in flight
+      rows[u] = (t0 + u * c.G < nt) ? (t0 + u * c.G) * M::RB + gl : c.n;
+      if (rows[u] < c.n) {
+        const size_t o = (size_t)rows[u] * KP + glane * M::CPL;
+        ld_cols<M::CPL>(P + o, p[u]);
+        if (anyx) ld_cols<M::CPL>(X + o, x[u]);
+        if (anyp) {
+          ld_cols<M::CPL>(R + o, r[u]);
+          dd[u] = __ldg(d + rows[u]);
+        }
+      }
     }
-    if (anyp) {
-      double r[M::CPL];
-      ld_cols<M::CPL>(R + o, r);
-      const double dd = __ldg(d + row);
 #pragma unroll
-      for (int k = 0; k < M::CPL; ++k)
-        if (pm[k]) p[k] = r[k] / dd + be[k] * p[k];
-      st_cols<M::CPL>(P + o, p);
+    for (int u = 0; u < U; ++u) {
+      if (rows[u] >= c.n) continue;
+      const size_t o = (size_t)rows[u] * KP + glane * M::CPL;
+      if (anyx) {
+#pragma unroll
+        for (int k = 0; k < M::CPL; ++k)
+          if (xm[k]) x[u][k] = x[u][k] + al[k] * p[u][k];
+        st_cols<M::CPL>(X + o, x[u]);
+      }
+      if (anyp) {
+#pragma unroll
+        for (int k = 0; k < M::CPL; ++k)
+          if (pm[k]) p[u][k] = r[u][k] / dd[u] + be[k] * p[u][k];
+        st_cols<M::CPL>(P + o, p[u]);
+      }
     }
   }
 }
@@ -501,10 +723,11 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
 // s = b - A x for CHECK columns (into Q), true residual, DONE / FAILED / REPLACE
 // (solver.py:94-102)
 template <int KP>
-__global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
+__global__ void __launch_bounds__(BLOCK, SPMM_BLOCKS_PER_SM)
     k_spmm_resid(Ctl c, Csr A, const double* __restrict__ B, const double* __restrict__ X,
                  double* __restrict__ Q) {
   using M = Map<KP>;
+  constexpr int R = Spmm<KP>::R;
   __shared__ double sm[M::RED];
   __shared__ double tot[KP];
   __shared__ int s_act[KP];
@@ -522,30 +745,28 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
     act[k] = s_act[glane * M::CPL + k];
     any |= act[k];
   }
-  const int rpb = rows_per_block(c.n, c.G);
-  const int r0 = blockIdx.x * rpb, r1 = min(c.n, r0 + rpb);
+  const int nt = n_tiles(c.n, M::RB);
   double v[1][M::CPL];
 #pragma unroll
   for (int k = 0; k < M::CPL; ++k) v[0][k] = 0.0;
-  for (int base = r0; base < r1; base += M::RB) {
-    const int row = base + gl;
-    const bool valid = row < r1;
-    double acc[M::CPL];
-    row_gather<KP>(A, X, row, valid, any, acc);
-    if (valid && any) {
-      const size_t o = (size_t)row * KP + glane * M::CPL;
+  spmm_sweep<KP>(c, A, X, any, [&](const int (&row)[R], double (&acc)[R][M::CPL]) {
+    if (!any) return;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (row[r] < 0) continue;
+      const size_t o = (size_t)row[r] * KP + glane * M::CPL;
       double b[M::CPL], q[M::CPL];
       ld_cols<M::CPL>(B + o, b);
       ld_cols<M::CPL>(Q + o, q);
 #pragma unroll
       for (int k = 0; k < M::CPL; ++k)
         if (act[k]) {
-          q[k] = b[k] - acc[k];
+          q[k] = b[k] - acc[r][k];
           v[0][k] += q[k] * q[k];
         }
       st_cols<M::CPL>(Q + o, q);
     }
-  }
+  });
   block_partials<KP, 1>(v, sm, c.part0, nullptr);
   if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
   if (tid < KP) {
@@ -589,13 +810,14 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
     act[k] = s_act[glane * M::CPL + k];
     any |= act[k];
   }
-  const int rpb = rows_per_block(c.n, c.G);
-  const int r0 = blockIdx.x * rpb, r1 = min(c.n, r0 + rpb);
+  const int nt = n_tiles(c.n, M::RB);
   double v[1][M::CPL];
 #pragma unroll
   for (int k = 0; k < M::CPL; ++k) v[0][k] = 0.0;
   if (any) {
-    for (int row = r0 + gl; row < r1; row += M::RB) {
+    for (int t = blockIdx.x; t < nt; t += c.G) {
+      const int row = t * M::RB + gl;
+      if (row >= c.n) continue;
       const size_t o = (size_t)row * KP + glane * M::CPL;
       double r[M::CPL], q[M::CPL];
       ld_cols<M::CPL>(R + o, r);
@@ -631,10 +853,10 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
 
 // ---------------------------------------------------------------- host driver
 
-inline int grid_for(int n, int kp) {
+inline int grid_for(int n, int kp, int blocks_per_sm = BLOCKS_PER_SM) {
   const int lpr = (kp / 2 < 32) ? kp / 2 : 32;
   const int rb = BLOCK / lpr;
-  int g = sm_count() * BLOCKS_PER_SM;
+  int g = sm_count() * blocks_per_sm;
   const int need = (n + rb - 1) / rb;
   if (need < g) g = need;
   return g < 1 ? 1 : g;
@@ -713,6 +935,8 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
     c.freeze = L.freeze;
   }
   Csr csr{A->indptr, A->indices, A->val};
+  Ctl cs = c;  // the SpMM kernels run their own grid (one block per SM)
+  cs.G = grid_for(n, KP, SPMM_BLOCKS_PER_SM);
   HF_CUDA(cudaMemsetAsync(L.counter, 0, sizeof(unsigned int) * 4, stream));
   k_init<KP><<<c.G, BLOCK, 0, stream>>>(c, B, d, X, L.R, L.P);
   HF_LAUNCH_CHECK();
@@ -743,11 +967,11 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
     HF_CUDA(cudaStreamCreateWithFlags(&guard.cs, cudaStreamNonBlocking));
     HF_CUDA(cudaStreamBeginCapture(guard.cs, cudaStreamCaptureModeThreadLocal));
     for (int r = 0; r < CHUNK; ++r) {
-      k_spmm_pq<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, csr, L.P, L.Q);
+      k_spmm_pq<KP><<<cs.G, BLOCK, 0, guard.cs>>>(cs, csr, L.P, L.Q);
       k_update_r<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, L.Q, L.R, d);
       k_update_xp<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, SUM_MASKED, X, L.P, L.R, d);
     }
-    k_spmm_resid<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, csr, B, X, L.Q);
+    k_spmm_resid<KP><<<cs.G, BLOCK, 0, guard.cs>>>(cs, csr, B, X, L.Q);
     k_replace<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, L.Q, L.R, d);
     k_update_xp<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, SUM_REPLACE, X, L.P, L.R, d);
     cudaMemcpyAsync(h_sum, L.summary, sizeof(int) * SUM_N, cudaMemcpyDeviceToHost, guard.cs);
@@ -819,6 +1043,8 @@ int profile(const hf_csr* A, const double* d, const double* B, int n, int rounds
   c.freeze = nullptr; c.part0 = L.part0; c.part1 = L.part1; c.counter = L.counter;
   c.summary = L.summary;
   Csr csr{A->indptr, A->indices, A->val};
+  Ctl cs = c;  // the SpMM kernels run their own grid (one block per SM)
+  cs.G = grid_for(n, KP, SPMM_BLOCKS_PER_SM);
   HF_CUDA(cudaMemsetAsync(L.counter, 0, sizeof(unsigned int) * 4, stream));
   k_init<KP><<<c.G, BLOCK, 0, stream>>>(c, B, d, X, L.R, L.P);
   HF_LAUNCH_CHECK();
@@ -828,7 +1054,7 @@ int profile(const hf_csr* A, const double* d, const double* B, int n, int rounds
   double acc[3] = {0, 0, 0};
   for (int r = 0; r < rounds; ++r) {
     cudaEventRecord(ev[0], stream);
-    k_spmm_pq<KP><<<c.G, BLOCK, 0, stream>>>(c, csr, L.P, L.Q);
+    k_spmm_pq<KP><<<cs.G, BLOCK, 0, stream>>>(cs, csr, L.P, L.Q);
     cudaEventRecord(ev[1], stream);
     k_update_r<KP><<<c.G, BLOCK, 0, stream>>>(c, L.Q, L.R, d);
     cudaEventRecord(ev[2], stream);

@@ -100,13 +100,12 @@ constexpr int ES_EB = 8;         // elements staged per batch
 constexpr int ES_MAXO = 16;      // outputs per thread per CTA (P*L chunk <= 4096)
 constexpr int ES_CHUNK = ES_THREADS * ES_MAXO;
 
-__device__ __forceinline__ double det3(const double a[3][3]) {
-  return a[0][0] * (a[1][1] * a[2][2] - a[1][2] * a[2][1]) -
-         a[0][1] * (a[1][0] * a[2][2] - a[1][2] * a[2][0]) +
-         a[0][2] * (a[1][0] * a[2][1] - a[1][1] * a[2][0]);
-}
+#define MUL(a, b) __dmul_rn((a), (b))
+#define ADD(a, b) __dadd_rn((a), (b))
+#define SUB(a, b) __dsub_rn((a), (b))
 
-// unit-sigma block of element e with grounded rows/cols zeroed (leadfield.py:189-196)
+// unit-sigma block of an element with grounded rows/cols zeroed
+// (leadfield.py:189-196); same explicitly rounded arithmetic as hf_p1_blocks.
 __device__ void unit_block(const double* __restrict__ nodes, const int32_t* __restrict__ conn,
                            int ground, double K[16]) {
   double p[4][3];
@@ -114,22 +113,26 @@ __device__ void unit_block(const double* __restrict__ nodes, const int32_t* __re
     for (int r = 0; r < 3; ++r) p[a][r] = nodes[3 * (size_t)conn[a] + r];
   double J[3][3];
   for (int r = 0; r < 3; ++r)
-    for (int k = 0; k < 3; ++k) J[r][k] = p[k + 1][r] - p[0][r];
-  const double det = det3(J), id = 1.0 / det, vol = det / 6.0;
+    for (int k = 0; k < 3; ++k) J[r][k] = SUB(p[k + 1][r], p[0][r]);
+  const double c0 = SUB(MUL(J[1][1], J[2][2]), MUL(J[1][2], J[2][1]));
+  const double c1 = SUB(MUL(J[1][0], J[2][2]), MUL(J[1][2], J[2][0]));
+  const double c2 = SUB(MUL(J[1][0], J[2][1]), MUL(J[1][1], J[2][0]));
+  const double det = ADD(SUB(MUL(J[0][0], c0), MUL(J[0][1], c1)), MUL(J[0][2], c2));
+  const double vol = __ddiv_rn(det, 6.0);
   double g[4][3];
-  g[1][0] = (J[1][1] * J[2][2] - J[1][2] * J[2][1]) * id;
-  g[1][1] = (J[0][2] * J[2][1] - J[0][1] * J[2][2]) * id;
-  g[1][2] = (J[0][1] * J[1][2] - J[0][2] * J[1][1]) * id;
-  g[2][0] = (J[1][2] * J[2][0] - J[1][0] * J[2][2]) * id;
-  g[2][1] = (J[0][0] * J[2][2] - J[0][2] * J[2][0]) * id;
-  g[2][2] = (J[0][2] * J[1][0] - J[0][0] * J[1][2]) * id;
-  g[3][0] = (J[1][0] * J[2][1] - J[1][1] * J[2][0]) * id;
-  g[3][1] = (J[0][1] * J[2][0] - J[0][0] * J[2][1]) * id;
-  g[3][2] = (J[0][0] * J[1][1] - J[0][1] * J[1][0]) * id;
-  for (int k = 0; k < 3; ++k) g[0][k] = -(g[1][k] + g[2][k] + g[3][k]);
+  g[1][0] = __ddiv_rn(SUB(MUL(J[1][1], J[2][2]), MUL(J[1][2], J[2][1])), det);
+  g[1][1] = __ddiv_rn(SUB(MUL(J[0][2], J[2][1]), MUL(J[0][1], J[2][2])), det);
+  g[1][2] = __ddiv_rn(SUB(MUL(J[0][1], J[1][2]), MUL(J[0][2], J[1][1])), det);
+  g[2][0] = __ddiv_rn(SUB(MUL(J[1][2], J[2][0]), MUL(J[1][0], J[2][2])), det);
+  g[2][1] = __ddiv_rn(SUB(MUL(J[0][0], J[2][2]), MUL(J[0][2], J[2][0])), det);
+  g[2][2] = __ddiv_rn(SUB(MUL(J[0][2], J[1][0]), MUL(J[0][0], J[1][2])), det);
+  g[3][0] = __ddiv_rn(SUB(MUL(J[1][0], J[2][1]), MUL(J[1][1], J[2][0])), det);
+  g[3][1] = __ddiv_rn(SUB(MUL(J[0][1], J[2][0]), MUL(J[0][0], J[2][1])), det);
+  g[3][2] = __ddiv_rn(SUB(MUL(J[0][0], J[1][1]), MUL(J[0][1], J[1][0])), det);
+  for (int k = 0; k < 3; ++k) g[0][k] = -ADD(ADD(g[1][k], g[2][k]), g[3][k]);
   for (int i = 0; i < 4; ++i)
     for (int j = 0; j < 4; ++j) {
-      double v = (g[i][0] * g[j][0] + g[i][1] * g[j][1] + g[i][2] * g[j][2]) * (vol * 1.0);
+      double v = MUL(ADD(ADD(MUL(g[i][0], g[j][0]), MUL(g[i][1], g[j][1])), MUL(g[i][2], g[j][2])), vol);
       if (conn[i] == ground || conn[j] == ground) v = 0.0;
       K[4 * i + j] = v;
     }

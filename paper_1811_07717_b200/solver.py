@@ -12,6 +12,7 @@ columns share a batch.
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -22,7 +23,7 @@ from . import _native as N
 from .device import DeviceCsr, PcgOperator, device, ldp_device, width_for
 from .errors import ConvergenceError, ParameterError, SingularPreconditionerError
 
-MAX_BATCH = 64  # RHS columns per multi-RHS solve (n x 64 fp64 = 512 B per node)
+MAX_BATCH = int(os.environ.get("HFB200_MAX_BATCH", "32"))  # RHS columns per multi-RHS solve
 
 
 @dataclass(frozen=True)
