@@ -1,0 +1,165 @@
+"""Host-side logic on CPU: the C-ABI library loads and exports every symbol the
+header declares; the input builders mirror the reference bit for bit; config
+validation and sharding arithmetic."""
+import hashlib
+import os
+import re
+
+import numpy as np
+import pytest
+
+from tests.fixtures import csr, electrodes_from_fixture, load, mesh_from_fixture
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def header_symbols():
+    text = open(os.path.join(ROOT, "include", "hfb200.h")).read()
+    return sorted(set(re.findall(r"\b(hf_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1811_07717_b200 import _native as N
+
+    declared = header_symbols()
+    assert len(declared) >= 17
+    for name in declared:
+        assert hasattr(N.lib, name), name
+    assert sorted(N.EXPORTED) == declared
+    assert N.lib.hf_version().decode().startswith("hfb200")
+
+
+def test_library_is_sm100a():
+    import subprocess
+
+    from paper_1811_07717_b200 import _native as N
+
+    out = subprocess.run(["cuobjdump", "--list-elf", N.LIB_PATH], capture_output=True, text=True)
+    if out.returncode != 0:
+        pytest.skip("cuobjdump unavailable")
+    assert "sm_100a" in out.stdout
+
+
+def test_workspace_queries_need_no_gpu():
+    from paper_1811_07717_b200 import _native as N
+
+    assert N.lib.hf_pcg_workspace_bytes(1000, 32) > 1000 * 32 * 8 * 3
+    assert N.lib.hf_p1_assemble_workspace_bytes(1000, 5000, 10) > 0
+    assert N.lib.hf_csr_prune_workspace_bytes(1000) > 0
+
+
+def test_pcg_config_validation():
+    import paper_1811_07717_b200 as eng
+
+    for kw in ({"tolerance": 0.0}, {"max_iterations": 0}, {"preconditioner": "amg"}):
+        with pytest.raises(eng.ParameterError):
+            eng.PcgConfig(**kw)
+    assert eng.PcgConfig().resolve_max_iterations(1_001_184) == 6002  # int(5 sqrt n) + 1000
+
+
+@pytest.mark.parametrize("name", ["sphere_small.npz", "layered_h12.npz", "layered_h14_tensor.npz",
+                                  "c1.npz"])
+def test_boundary_ground_and_B_match_reference(name):
+    from paper_1811_07717_b200 import model
+
+    fx = load(name)
+    mesh = mesh_from_fixture(fx)
+    bf, ow = mesh.boundary_triangles()
+    assert sha(bf.astype(np.int64)) == str(fx["bfaces_sha"])
+    assert sha(ow.astype(np.int64)) == str(fx["bowners_sha"])
+    el = electrodes_from_fixture(mesh, fx)
+    assert model.ground_node(mesh, el) == int(fx["ground"])
+    B, C, R = model.assemble_B_C_R(mesh, el)
+    assert (B != csr(fx, "B")).nnz == 0
+    np.testing.assert_array_equal(C.diagonal(), fx["Cdiag"])
+
+
+@pytest.mark.parametrize("name", ["sphere_small.npz", "layered_h12.npz", "c1.npz"])
+def test_assemble_G_matches_reference(name):
+    """Vectorised Whitney source matrix: same pattern, values to rounding."""
+    from paper_1811_07717_b200 import model
+
+    fx = load(name)
+    mesh = mesh_from_fixture(fx)
+    src = model.SourceSpace(positions=fx["src_positions"], orientations=None,
+                            element_ids=fx["src_elements"], mode="unconstrained")
+    G = model.assemble_G(mesh, src)
+    Gr = csr(fx, "G").copy()
+    Gr.sort_indices()
+    np.testing.assert_array_equal(G.indptr, Gr.indptr)
+    np.testing.assert_array_equal(G.indices, Gr.indices)
+    np.testing.assert_allclose(G.data, Gr.data, rtol=1e-9, atol=1e-13 * np.abs(Gr.data).max())
+
+
+def test_electrodes_from_centers_match_reference():
+    from paper_1811_07717_b200 import model, synthetic
+
+    fx = load("layered_h12.npz")
+    mesh = mesh_from_fixture(fx)
+    el = model.ElectrodeSet.from_centers(mesh, synthetic.fibonacci_sphere_points(16, 0.092),
+                                         radius=0.014, impedances=1e3)
+    ref = electrodes_from_fixture(mesh, fx)
+    for a, b in zip(el.triangle_ids, ref.triangle_ids):
+        np.testing.assert_array_equal(a, b)
+
+
+def test_dof_map_matches_reference_draws():
+    from paper_1811_07717_b200.leadfield import build_dof_map
+
+    fx = load("layered_h12.npz")
+    mesh = mesh_from_fixture(fx)
+    dofs = build_dof_map(mesh, [0, 1], 20, seed=2, chunk=64)  # tiny chunks: same answer
+    np.testing.assert_array_equal(np.concatenate(dofs.element_sets), fx["eit_dof_elems"])
+    np.testing.assert_array_equal(np.cumsum([0] + [len(e) for e in dofs.element_sets]),
+                                  fx["eit_dof_ptr"])
+    np.testing.assert_array_equal(dofs.centers, fx["eit_centers"])
+
+
+def test_column_blocks():
+    from paper_1811_07717_b200.engine import column_blocks
+
+    for L, w in [(128, 8), (128, 3), (5, 8), (256, 8)]:
+        b = column_blocks(L, w)
+        assert b[0][0] == 0 and b[-1][1] == L
+        assert all(b[i][1] == b[i + 1][0] for i in range(w - 1))
+        sizes = [c1 - c0 for c0, c1 in b]
+        assert max(sizes) - min(sizes) <= 1
+
+
+def test_synthetic_c1_mesh_is_a_valid_kuhn_grid():
+    from paper_1811_07717_b200 import synthetic
+
+    mesh = synthetic.sphere_mesh(synthetic.C1_RADII, synthetic.C1_COND, 0.012)
+    h = 0.012
+    np.testing.assert_allclose(mesh.volumes, h ** 3 / 6, rtol=1e-9)
+    assert set(np.unique(mesh.labels)) == {0, 1, 2}
+
+
+def test_install_rebinds_reference_entry_points():
+    """With the reference importable (this container), install() patches the
+    module attributes headfem resolves at call time and uninstall() restores."""
+    import sys
+
+    ref = "/root/reference/pkg/src"
+    if not os.path.isdir(ref):
+        pytest.skip("reference not present")
+    sys.path.insert(0, ref)
+    try:
+        import headfem
+        import headfem.leadfield as hl
+        import headfem.solver as hs
+
+        import paper_1811_07717_b200 as eng
+
+        orig = hs.pcg_solve
+        eng.install(headfem)
+        assert hs.pcg_solve is eng.pcg_solve and hl.transfer_matrix is eng.transfer_matrix
+        assert hl.eeg_leadfield is eng.eeg_leadfield
+        eng.uninstall()
+        assert hs.pcg_solve is orig
+    finally:
+        sys.path.remove(ref)
