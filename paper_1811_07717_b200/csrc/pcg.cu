@@ -60,6 +60,7 @@ struct Ctl {
   double *normb, *rz, *alpha, *beta, *best_res, *true_res;
   int *iters, *best_iter, *state, *xmask, *pmask, *freeze;
   double *part0, *part1;
+  double2* dd;  // per row {d_i, 1/d_i}, written by k_init
   unsigned int* counter;
   int* summary;
 };
@@ -72,14 +73,14 @@ struct Csr {
 
 template <int KP>
 struct Map {
-  static constexpr int LPR = (KP / 2 < 32) ? KP / 2 : 32;  // lanes per row
-  static constexpr int CPL = KP / LPR;                      // columns per lane (2 or 4)
+  static constexpr int CPL = (KP >= 4) ? 4 : 2;  // columns per lane: one 256-bit access
+  static constexpr int LPR = KP / CPL;            // lanes per row
   static constexpr int RB = BLOCK / LPR;                    // rows per block pass
   static constexpr int SPLIT = BLOCK / KP;                  // last-block reduction splits
   static constexpr int RED = (NWARP * KP > BLOCK) ? NWARP * KP : BLOCK;
   // row tiles in flight per thread in the streaming kernels (register budget: 64)
-  static constexpr int UR = 2;                                    // k_update_r
-  static constexpr int UX = (CPL == 4) ? 1 : 2;                   // k_update_xp
+  static constexpr int UR = (CPL == 4) ? 1 : 2;  // k_update_r
+  static constexpr int UX = (CPL == 4) ? 1 : 2;  // k_update_xp
 };
 
 // Rows are dealt to blocks in tiles of RB rows, round-robin (tile t -> block
@@ -88,31 +89,51 @@ struct Map {
 // per block made every block's neighbours far apart in time: 4x DRAM re-reads).
 __host__ __device__ inline int n_tiles(int n, int rb) { return (n + rb - 1) / rb; }
 
+// Column slices of a row move as one 256-bit access (LDG/STG.E.256 on
+// sm_100a) when a lane owns 4 columns, else as a 128-bit access.
 template <int CPL>
-__device__ __forceinline__ void ld_cols(const double* __restrict__ p, double (&v)[CPL]) {
-  const double2* q = reinterpret_cast<const double2*>(p);
-#pragma unroll
-  for (int h = 0; h < CPL / 2; ++h) {
-    double2 t = q[h];
-    v[2 * h] = t.x;
-    v[2 * h + 1] = t.y;
+__device__ __forceinline__ void ld_cols(const double* p, double (&v)[CPL]) {
+  if constexpr (CPL == 4) {
+    asm volatile("ld.global.v4.f64 {%0,%1,%2,%3}, [%4];"
+                 : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+                 : "l"(p));
+  } else {
+    const double2 t = *reinterpret_cast<const double2*>(p);
+    v[0] = t.x;
+    v[1] = t.y;
   }
 }
 template <int CPL>
 __device__ __forceinline__ void ldg_cols(const double* __restrict__ p, double (&v)[CPL]) {
-  const double2* q = reinterpret_cast<const double2*>(p);
-#pragma unroll
-  for (int h = 0; h < CPL / 2; ++h) {
-    double2 t = __ldg(q + h);
-    v[2 * h] = t.x;
-    v[2 * h + 1] = t.y;
+  if constexpr (CPL == 4) {
+    asm("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+        : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+        : "l"(p));
+  } else {
+    const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+    v[0] = t.x;
+    v[1] = t.y;
   }
 }
 template <int CPL>
 __device__ __forceinline__ void st_cols(double* p, const double (&v)[CPL]) {
-  double2* q = reinterpret_cast<double2*>(p);
-#pragma unroll
-  for (int h = 0; h < CPL / 2; ++h) q[h] = make_double2(v[2 * h], v[2 * h + 1]);
+  if constexpr (CPL == 4) {
+    asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]),
+                 "d"(v[2]), "d"(v[3])
+                 : "memory");
+  } else {
+    *reinterpret_cast<double2*>(p) = make_double2(v[0], v[1]);
+  }
+}
+
+// z = x / d with the row's precomputed reciprocal and one residual
+// correction (3 flops instead of a ~10-instruction fp64 division): the
+// corrected quotient is the correctly rounded x / d except in rare
+// double-rounding ties, where it is one ulp away.  dd = {d_i, 1/d_i}.
+__device__ __forceinline__ double zdiv(double x, double2 dd) {
+  const double q0 = x * dd.y;
+  const double res = fma(-q0, dd.x, x);
+  return fma(res, dd.y, q0);
 }
 
 // Sum NV per-column values over the block in a fixed order and store the
@@ -218,6 +239,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
     double b[M::CPL], z[M::CPL], zero[M::CPL];
     ld_cols<M::CPL>(B + o, b);
     const double dd = d[row];
+    if (glane == 0) c.dd[row] = make_double2(dd, 1.0 / dd);
 #pragma unroll
     for (int k = 0; k < M::CPL; ++k) {
       z[k] = b[k] / dd;
@@ -263,19 +285,17 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
 // The SpMM kernels are latency-bound gathers: they run one 512-thread block
 // per SM with a 128-register budget and keep R rows x GB gathers in flight
 // per lane group (all loads issued before any FMA consumes them).
-#ifndef HF_SPMM_BPS
-#define HF_SPMM_BPS 2
-#endif
-constexpr int SPMM_BLOCKS_PER_SM = HF_SPMM_BPS;
 constexpr int GB = 8;  // gathers per batch
 
 template <int KP>
 struct Spmm {
-#ifndef HF_SPMM_R2
-  static constexpr int R = 1;  // rows in flight per row group (pipelined across steps)
-#else
-  static constexpr int R = (Map<KP>::CPL == 4) ? 1 : 2;
-#endif
+  static constexpr int R = 1;  // rows per row group per step (pipelined across steps)
+  // 4-column lanes hold 8 x 256-bit gathers in registers: one block per SM
+  // with a 128-register budget; 2-column lanes fit two blocks per SM.
+  static constexpr int BPS = (Map<KP>::CPL == 4) ? 1 : 2;
+  // (index, value) pairs each lane of a row group holds for the pipeline
+  static constexpr int EPL = (Map<KP>::LPR >= 16) ? 1 : 2;
+  static constexpr bool PIPELINED = Map<KP>::LPR >= 8;
 };
 
 // acc[r] = sum_j a_ij * V[col_j, lane columns] for the R rows of this row group.
@@ -388,27 +408,33 @@ __device__ __forceinline__ void load_meta(const Ctl& c, const Csr& A, int t0, in
 
 template <int KP, int R>
 __device__ __forceinline__ void load_entries(const Csr& A, const int (&st)[R], const int (&ln)[R],
-                                             int (&ci)[R], double (&cv)[R]) {
-  const int glane = threadIdx.x % Map<KP>::LPR;
+                                             int (&ci)[R][Spmm<KP>::EPL],
+                                             double (&cv)[R][Spmm<KP>::EPL]) {
+  constexpr int LPR = Map<KP>::LPR;
+  const int glane = threadIdx.x % LPR;
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    ci[r] = 0;
-    cv[r] = 0.0;
-    if (glane < ln[r]) {
-      ci[r] = __ldg(A.indices + st[r] + glane);
-      cv[r] = __ldg(A.val + st[r] + glane);
+  for (int r = 0; r < R; ++r)
+#pragma unroll
+    for (int q = 0; q < Spmm<KP>::EPL; ++q) {
+      const int e = q * LPR + glane;
+      ci[r][q] = 0;
+      cv[r][q] = 0.0;
+      if (e < ln[r]) {
+        ci[r][q] = __ldg(A.indices + st[r] + e);
+        cv[r][q] = __ldg(A.val + st[r] + e);
+      }
     }
-  }
 }
 
 template <int KP, class Epi>
 __device__ __forceinline__ void spmm_sweep(const Ctl& c, const Csr& A, const double* __restrict__ V,
                                            bool any, Epi&& epi) {
   using M = Map<KP>;
-  constexpr int R = Spmm<KP>::R, LPR = M::LPR, CPL = M::CPL;
+  constexpr int R = Spmm<KP>::R, LPR = M::LPR, CPL = M::CPL, EPL = Spmm<KP>::EPL;
+  constexpr int CAP = LPR * EPL;  // entries per row served from registers
   const int nt = n_tiles(c.n, M::RB);
   const int step = R * c.G;
-  if constexpr (LPR < 16) {
+  if constexpr (!Spmm<KP>::PIPELINED) {
     const int gl = threadIdx.x / LPR;
     for (int t0 = blockIdx.x; t0 < nt; t0 += step) {
       int row[R];
@@ -424,17 +450,17 @@ __device__ __forceinline__ void spmm_sweep(const Ctl& c, const Csr& A, const dou
   } else {
     const int glane = threadIdx.x % LPR;
     const double* __restrict__ Vl = V + glane * CPL;
-    int row[R], st[R], ln[R], ci[R];
-    double cv[R];
+    int row[R], st[R], ln[R], ci[R][EPL];
+    double cv[R][EPL];
     int rowN[R], stN[R], lnN[R];
     int t0 = blockIdx.x;
     load_meta<KP, R>(c, A, t0, nt, row, st, ln);
     load_entries<KP, R>(A, st, ln, ci, cv);
     load_meta<KP, R>(c, A, t0 + step, nt, rowN, stN, lnN);
     for (; t0 < nt; t0 += step) {
-      int ciN[R], rowNN[R], stNN[R], lnNN[R];
-      double cvN[R];
-      load_entries<KP, R>(A, stN, lnN, ciN, cvN);                 // step s+1 pairs
+      int ciN[R][EPL], rowNN[R], stNN[R], lnNN[R];
+      double cvN[R][EPL];
+      load_entries<KP, R>(A, stN, lnN, ciN, cvN);                   // step s+1 pairs
       load_meta<KP, R>(c, A, t0 + 2 * step, nt, rowNN, stNN, lnNN);  // step s+2 pointers
       double acc[R][CPL];
       int maxlen = 0;
@@ -445,38 +471,43 @@ __device__ __forceinline__ void spmm_sweep(const Ctl& c, const Csr& A, const dou
         maxlen = max(maxlen, ln[r]);
       }
       if (LPR < 32) maxlen = (int)__reduce_max_sync(FULL, (unsigned)maxlen);
-      const int inreg = min(maxlen, LPR);
-      for (int b = 0; b < inreg; b += GB) {
-        double g[R][GB][CPL];
+      int lim[R];  // entries this lane group gathers from registers (0 if no active column)
 #pragma unroll
-        for (int r = 0; r < R; ++r)
+      for (int r = 0; r < R; ++r) lim[r] = any ? min(ln[r], CAP) : 0;
+      const int inreg = min(maxlen, CAP);
+      // batches of GB entries: all GB gathers issued before the FMAs use them
 #pragma unroll
-          for (int t = 0; t < GB; ++t) {
-            const int e = b + t;
-            const int cc = __shfl_sync(FULL, ci[r], e & (LPR - 1), LPR);
-            if (e < LPR && e < ln[r] && any) {
-              ldg_cols<CPL>(Vl + (size_t)cc * KP, g[r][t]);
-            } else {
+      for (int q = 0; q < EPL; ++q) {
+        if (q * LPR >= inreg) break;
 #pragma unroll
-              for (int k = 0; k < CPL; ++k) g[r][t][k] = 0.0;
+        for (int b = 0; b < LPR; b += GB) {
+          if (q * LPR + b >= inreg) break;
+          double g[R][GB][CPL];
+#pragma unroll
+          for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int t = 0; t < GB; ++t) {
+              const int e = q * LPR + b + t;
+              const int cc = __shfl_sync(FULL, ci[r][q], (b + t) % LPR, LPR);
+              if (e < lim[r]) ldg_cols<CPL>(Vl + (size_t)cc * KP, g[r][t]);
             }
-          }
 #pragma unroll
-        for (int r = 0; r < R; ++r)
+          for (int r = 0; r < R; ++r)
 #pragma unroll
-          for (int t = 0; t < GB; ++t) {
-            const int e = b + t;
-            const double vv = __shfl_sync(FULL, cv[r], e & (LPR - 1), LPR);
-            if (e < LPR && e < ln[r]) {
+            for (int t = 0; t < GB; ++t) {
+              const int e = q * LPR + b + t;
+              const double vv = __shfl_sync(FULL, cv[r][q], (b + t) % LPR, LPR);
+              if (e < lim[r]) {
 #pragma unroll
-              for (int k = 0; k < CPL; ++k) acc[r][k] = fma(vv, g[r][t][k], acc[r][k]);
+                for (int k = 0; k < CPL; ++k) acc[r][k] = fma(vv, g[r][t][k], acc[r][k]);
+              }
             }
-          }
+        }
       }
-      if (maxlen > LPR) {  // long rows: remaining entries straight from memory
+      if (maxlen > CAP) {  // long rows: remaining entries straight from memory
 #pragma unroll
         for (int r = 0; r < R; ++r)
-          for (int e = LPR; e < ln[r]; ++e) {
+          for (int e = CAP; e < ln[r]; ++e) {
             const int cc = __ldg(A.indices + st[r] + e);
             const double vv = __ldg(A.val + st[r] + e);
             if (any) {
@@ -493,8 +524,11 @@ __device__ __forceinline__ void spmm_sweep(const Ctl& c, const Csr& A, const dou
         row[r] = rowN[r];
         st[r] = stN[r];
         ln[r] = lnN[r];
-        ci[r] = ciN[r];
-        cv[r] = cvN[r];
+#pragma unroll
+        for (int q = 0; q < EPL; ++q) {
+          ci[r][q] = ciN[r][q];
+          cv[r][q] = cvN[r][q];
+        }
         rowN[r] = rowNN[r];
         stN[r] = stNN[r];
         lnN[r] = lnNN[r];
@@ -505,7 +539,7 @@ __device__ __forceinline__ void spmm_sweep(const Ctl& c, const Csr& A, const dou
 
 // q = A p, partial p.q, alpha = rz / p.q       (solver.py:87-88)
 template <int KP>
-__global__ void __launch_bounds__(BLOCK, SPMM_BLOCKS_PER_SM)
+__global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
     k_spmm_pq(Ctl c, Csr A, const double* __restrict__ P, double* __restrict__ Q) {
   using M = Map<KP>;
   constexpr int R = Spmm<KP>::R;
@@ -551,7 +585,7 @@ __global__ void __launch_bounds__(BLOCK, SPMM_BLOCKS_PER_SM)
 // r -= alpha q ; res = |r|/|b| ; best ; tolerance / max_iter ; beta   (solver.py:90-106)
 template <int KP>
 __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
-    k_update_r(Ctl c, const double* __restrict__ Q, double* R, const double* __restrict__ d) {
+    k_update_r(Ctl c, const double* __restrict__ Q, double* R) {
   using M = Map<KP>;
   __shared__ double sm[2 * M::RED];
   __shared__ double tot[2 * KP];
@@ -584,7 +618,8 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
   if (any) {
     constexpr int U = M::UR;
     for (int t0 = blockIdx.x; t0 < nt; t0 += U * c.G) {
-      double r[U][M::CPL], q[U][M::CPL], dd[U];
+      double r[U][M::CPL], q[U][M::CPL];
+      double2 dd[U];
       int rows[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {  // all loads first: U rows in flight
@@ -593,7 +628,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
           const size_t o = (size_t)rows[u] * KP + glane * M::CPL;
           ld_cols<M::CPL>(R + o, r[u]);
           ld_cols<M::CPL>(Q + o, q[u]);
-          dd[u] = __ldg(d + rows[u]);
+          dd[u] = c.dd[rows[u]];
         }
       }
 #pragma unroll
@@ -604,7 +639,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
           if (act[k]) {
             r[u][k] = r[u][k] - al[k] * q[u][k];
             v[0][k] += r[u][k] * r[u][k];
-            v[1][k] += r[u][k] * (r[u][k] / dd[u]);
+            v[1][k] += r[u][k] * zdiv(r[u][k], dd[u]);
           }
         }
         st_cols<M::CPL>(R + (size_t)rows[u] * KP + glane * M::CPL, r[u]);
@@ -653,8 +688,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
 // x += alpha p (xmask) ; p = r/d + beta p (pmask)      (solver.py:89,103,107)
 template <int KP>
 __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
-    k_update_xp(Ctl c, int gate, double* X, double* P, const double* __restrict__ R,
-                const double* __restrict__ d) {
+    k_update_xp(Ctl c, int gate, double* X, double* P, const double* __restrict__ R) {
   using M = Map<KP>;
   __shared__ double s_alpha[KP], s_beta[KP];
   __shared__ int s_xm[KP], s_pm[KP];
@@ -684,7 +718,8 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
   const int nt = n_tiles(c.n, M::RB);
   constexpr int U = M::UX;
   for (int t0 = blockIdx.x; t0 < nt; t0 += U * c.G) {
-    double p[U][M::CPL], x[U][M::CPL], r[U][M::CPL], dd[U];
+    double p[U][M::CPL], x[U][M::CPL], r[U][M::CPL];
+    double2 dd[U];
     int rows[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {  // all loads first: U rows in flight
@@ -695,7 +730,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
         if (anyx) ld_cols<M::CPL>(X + o, x[u]);
         if (anyp) {
           ld_cols<M::CPL>(R + o, r[u]);
-          dd[u] = __ldg(d + rows[u]);
+          dd[u] = c.dd[rows[u]];
         }
       }
     }
@@ -712,7 +747,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
       if (anyp) {
 #pragma unroll
         for (int k = 0; k < M::CPL; ++k)
-          if (pm[k]) p[u][k] = r[u][k] / dd[u] + be[k] * p[u][k];
+          if (pm[k]) p[u][k] = zdiv(r[u][k], dd[u]) + be[k] * p[u][k];
         st_cols<M::CPL>(P + o, p[u]);
       }
     }
@@ -723,7 +758,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
 // s = b - A x for CHECK columns (into Q), true residual, DONE / FAILED / REPLACE
 // (solver.py:94-102)
 template <int KP>
-__global__ void __launch_bounds__(BLOCK, SPMM_BLOCKS_PER_SM)
+__global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
     k_spmm_resid(Ctl c, Csr A, const double* __restrict__ B, const double* __restrict__ X,
                  double* __restrict__ Q) {
   using M = Map<KP>;
@@ -794,7 +829,7 @@ __global__ void __launch_bounds__(BLOCK, SPMM_BLOCKS_PER_SM)
 // r = s for REPLACE columns, rz_next = r.(r/d), beta, resume   (solver.py:101-106)
 template <int KP>
 __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
-    k_replace(Ctl c, const double* __restrict__ Q, double* R, const double* __restrict__ d) {
+    k_replace(Ctl c, const double* __restrict__ Q, double* R) {
   using M = Map<KP>;
   __shared__ double sm[M::RED];
   __shared__ double tot[KP];
@@ -822,12 +857,12 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
       double r[M::CPL], q[M::CPL];
       ld_cols<M::CPL>(R + o, r);
       ld_cols<M::CPL>(Q + o, q);
-      const double dd = __ldg(d + row);
+      const double2 dd = c.dd[row];
 #pragma unroll
       for (int k = 0; k < M::CPL; ++k)
         if (act[k]) {
           r[k] = q[k];
-          v[0][k] += r[k] * (r[k] / dd);
+          v[0][k] += r[k] * zdiv(r[k], dd);
         }
       st_cols<M::CPL>(R + o, r);
     }
@@ -854,7 +889,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
 // ---------------------------------------------------------------- host driver
 
 inline int grid_for(int n, int kp, int blocks_per_sm = BLOCKS_PER_SM) {
-  const int lpr = (kp / 2 < 32) ? kp / 2 : 32;
+  const int lpr = (kp >= 4) ? kp / 4 : kp / 2;
   const int rb = BLOCK / lpr;
   int g = sm_count() * blocks_per_sm;
   const int need = (n + rb - 1) / rb;
@@ -864,6 +899,7 @@ inline int grid_for(int n, int kp, int blocks_per_sm = BLOCKS_PER_SM) {
 
 struct Layout {
   double *R, *P, *Q, *part0, *part1;
+  double2* dd;
   double *normb, *rz, *alpha, *beta, *best_res, *true_res;
   int *iters, *best_iter, *state, *xmask, *pmask, *freeze;
   unsigned int* counter;
@@ -881,6 +917,7 @@ inline Layout carve(void* ws, int n, int kp) {
   L.Q = cv.take<double>(nk);
   L.part0 = cv.take<double>((size_t)gmax * kp);
   L.part1 = cv.take<double>((size_t)gmax * kp);
+  L.dd = cv.take<double2>((size_t)n);
   L.normb = cv.take<double>(kp);
   L.rz = cv.take<double>(kp);
   L.alpha = cv.take<double>(kp);
@@ -928,6 +965,7 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
   c.freeze = nullptr;
   c.part0 = L.part0;
   c.part1 = L.part1;
+  c.dd = L.dd;
   c.counter = L.counter;
   c.summary = L.summary;
   if (freeze_at != nullptr) {
@@ -936,7 +974,7 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
   }
   Csr csr{A->indptr, A->indices, A->val};
   Ctl cs = c;  // the SpMM kernels run their own grid (one block per SM)
-  cs.G = grid_for(n, KP, SPMM_BLOCKS_PER_SM);
+  cs.G = grid_for(n, KP, Spmm<KP>::BPS);
   HF_CUDA(cudaMemsetAsync(L.counter, 0, sizeof(unsigned int) * 4, stream));
   k_init<KP><<<c.G, BLOCK, 0, stream>>>(c, B, d, X, L.R, L.P);
   HF_LAUNCH_CHECK();
@@ -968,12 +1006,12 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
     HF_CUDA(cudaStreamBeginCapture(guard.cs, cudaStreamCaptureModeThreadLocal));
     for (int r = 0; r < CHUNK; ++r) {
       k_spmm_pq<KP><<<cs.G, BLOCK, 0, guard.cs>>>(cs, csr, L.P, L.Q);
-      k_update_r<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, L.Q, L.R, d);
-      k_update_xp<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, SUM_MASKED, X, L.P, L.R, d);
+      k_update_r<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, L.Q, L.R);
+      k_update_xp<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, SUM_MASKED, X, L.P, L.R);
     }
     k_spmm_resid<KP><<<cs.G, BLOCK, 0, guard.cs>>>(cs, csr, B, X, L.Q);
-    k_replace<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, L.Q, L.R, d);
-    k_update_xp<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, SUM_REPLACE, X, L.P, L.R, d);
+    k_replace<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, L.Q, L.R);
+    k_update_xp<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, SUM_REPLACE, X, L.P, L.R);
     cudaMemcpyAsync(h_sum, L.summary, sizeof(int) * SUM_N, cudaMemcpyDeviceToHost, guard.cs);
     cudaError_t ce = cudaStreamEndCapture(guard.cs, &guard.g);
     if (ce != cudaSuccess) {
@@ -1040,11 +1078,11 @@ int profile(const hf_csr* A, const double* d, const double* B, int n, int rounds
   c.normb = L.normb; c.rz = L.rz; c.alpha = L.alpha; c.beta = L.beta;
   c.best_res = L.best_res; c.true_res = L.true_res; c.iters = L.iters;
   c.best_iter = L.best_iter; c.state = L.state; c.xmask = L.xmask; c.pmask = L.pmask;
-  c.freeze = nullptr; c.part0 = L.part0; c.part1 = L.part1; c.counter = L.counter;
+  c.freeze = nullptr; c.part0 = L.part0; c.part1 = L.part1; c.dd = L.dd; c.counter = L.counter;
   c.summary = L.summary;
   Csr csr{A->indptr, A->indices, A->val};
   Ctl cs = c;  // the SpMM kernels run their own grid (one block per SM)
-  cs.G = grid_for(n, KP, SPMM_BLOCKS_PER_SM);
+  cs.G = grid_for(n, KP, Spmm<KP>::BPS);
   HF_CUDA(cudaMemsetAsync(L.counter, 0, sizeof(unsigned int) * 4, stream));
   k_init<KP><<<c.G, BLOCK, 0, stream>>>(c, B, d, X, L.R, L.P);
   HF_LAUNCH_CHECK();
@@ -1056,9 +1094,9 @@ int profile(const hf_csr* A, const double* d, const double* B, int n, int rounds
     cudaEventRecord(ev[0], stream);
     k_spmm_pq<KP><<<cs.G, BLOCK, 0, stream>>>(cs, csr, L.P, L.Q);
     cudaEventRecord(ev[1], stream);
-    k_update_r<KP><<<c.G, BLOCK, 0, stream>>>(c, L.Q, L.R, d);
+    k_update_r<KP><<<c.G, BLOCK, 0, stream>>>(c, L.Q, L.R);
     cudaEventRecord(ev[2], stream);
-    k_update_xp<KP><<<c.G, BLOCK, 0, stream>>>(c, SUM_MASKED, X, L.P, L.R, d);
+    k_update_xp<KP><<<c.G, BLOCK, 0, stream>>>(c, SUM_MASKED, X, L.P, L.R);
     cudaEventRecord(ev[3], stream);
     HF_CUDA(cudaEventSynchronize(ev[3]));
     for (int k = 0; k < 3; ++k) {

@@ -23,7 +23,7 @@ from . import _native as N
 from .device import DeviceCsr, PcgOperator, device, ldp_device, width_for
 from .errors import ConvergenceError, ParameterError, SingularPreconditionerError
 
-MAX_BATCH = int(os.environ.get("HFB200_MAX_BATCH", "32"))  # RHS columns per multi-RHS solve
+MAX_BATCH = int(os.environ.get("HFB200_MAX_BATCH", "64"))  # RHS columns per multi-RHS solve
 
 
 @dataclass(frozen=True)
