@@ -119,6 +119,17 @@ def test_dof_map_matches_reference_draws():
     np.testing.assert_array_equal(dofs.centers, fx["eit_centers"])
 
 
+def test_dof_map_tree_path_matches_reference():
+    from paper_1811_07717_b200.leadfield import build_dof_map
+
+    fx = load("layered_h12.npz")
+    mesh = mesh_from_fixture(fx)
+    dofs = build_dof_map(mesh, [0, 1], 20, seed=2, method="tree")
+    np.testing.assert_array_equal(np.concatenate(dofs.element_sets), fx["eit_dof_elems"])
+    np.testing.assert_array_equal(np.cumsum([0] + [len(e) for e in dofs.element_sets]),
+                                  fx["eit_dof_ptr"])
+
+
 def test_column_blocks():
     from paper_1811_07717_b200.engine import column_blocks
 
