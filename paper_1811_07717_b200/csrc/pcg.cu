@@ -450,18 +450,38 @@ __device__ __forceinline__ void spmm_sweep(const Ctl& c, const Csr& A, const dou
   } else {
     const int glane = threadIdx.x % LPR;
     const double* __restrict__ Vl = V + glane * CPL;
+    // pipeline: row pointers 3 steps ahead, (index, value) pairs 2 steps
+    // ahead, and one step ahead an L2 bulk prefetch of each row's largest-index
+    // neighbour (on a grid-ordered mesh the +z neighbour: the row this sweep
+    // touches first, i.e. the DRAM miss), then the gathers of the current step.
     int row[R], st[R], ln[R], ci[R][EPL];
     double cv[R][EPL];
-    int rowN[R], stN[R], lnN[R];
+    int rowN[R], stN[R], lnN[R], ciN[R][EPL];
+    double cvN[R][EPL];
+    int rowNN[R], stNN[R], lnNN[R];
     int t0 = blockIdx.x;
     load_meta<KP, R>(c, A, t0, nt, row, st, ln);
     load_entries<KP, R>(A, st, ln, ci, cv);
     load_meta<KP, R>(c, A, t0 + step, nt, rowN, stN, lnN);
+    load_entries<KP, R>(A, stN, lnN, ciN, cvN);
+    load_meta<KP, R>(c, A, t0 + 2 * step, nt, rowNN, stNN, lnNN);
     for (; t0 < nt; t0 += step) {
-      int ciN[R][EPL], rowNN[R], stNN[R], lnNN[R];
-      double cvN[R][EPL];
-      load_entries<KP, R>(A, stN, lnN, ciN, cvN);                   // step s+1 pairs
-      load_meta<KP, R>(c, A, t0 + 2 * step, nt, rowNN, stNN, lnNN);  // step s+2 pointers
+      int ciNN[R][EPL], rowN3[R], stN3[R], lnN3[R];
+      double cvNN[R][EPL];
+      load_entries<KP, R>(A, stNN, lnNN, ciNN, cvNN);               // step s+2 pairs
+      load_meta<KP, R>(c, A, t0 + 3 * step, nt, rowN3, stN3, lnN3);  // step s+3 pointers
+      if (any) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int e = lnN[r] - 1;  // sorted columns: the last entry is the largest index
+          if (e >= 0 && e < CAP && glane == e % LPR) {
+            const int cc = (e / LPR == 0) ? ciN[r][0] : ciN[r][EPL - 1];
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(V + (size_t)cc * KP),
+                         "r"(KP * 8)
+                         : "memory");
+          }
+        }
+      }
       double acc[R][CPL];
       int maxlen = 0;
 #pragma unroll
@@ -528,10 +548,15 @@ __device__ __forceinline__ void spmm_sweep(const Ctl& c, const Csr& A, const dou
         for (int q = 0; q < EPL; ++q) {
           ci[r][q] = ciN[r][q];
           cv[r][q] = cvN[r][q];
+          ciN[r][q] = ciNN[r][q];
+          cvN[r][q] = cvNN[r][q];
         }
         rowN[r] = rowNN[r];
         stN[r] = stNN[r];
         lnN[r] = lnNN[r];
+        rowNN[r] = rowN3[r];
+        stNN[r] = stN3[r];
+        lnNN[r] = lnN3[r];
       }
     }
   }
