@@ -137,14 +137,22 @@ def kernel_roofline(engine, A, rounds=20):
     X = torch.empty_like(Bb)
     ws = torch.empty(N.lib.hf_pcg_workspace_bytes(n, kp), dtype=torch.uint8, device=Bb.device)
     ms = (N.C.c_float * 3)()
+    fused = N.C.c_int32(0)
     N.check("hf_pcg_profile", N.lib.hf_pcg_profile(
-        N.C.byref(op.Ac.struct), N.ptr(op.d), N.ptr(Bb), n, kp, rounds, N.ptr(X), ms, N.ptr(ws),
-        ws.numel(), N.stream_handle()))
+        N.C.byref(op.Ac.struct), N.ptr(op.d), N.ptr(Bb), n, kp, rounds, N.ptr(X), ms,
+        N.C.byref(fused), N.ptr(ws), ws.numel(), N.stream_handle()))
     nnz = op.Ac.nnz
-    algo = {"k_spmm_pq": 16 * n * kp + 12 * nnz + 4 * (n + 1),
-            "k_update_r": 24 * n * kp + 8 * n,
-            "k_update_xp": 40 * n * kp + 8 * n}
-    times = dict(zip(algo, [float(ms[0]), float(ms[1]), float(ms[2])]))
+    if fused.value:
+        # k_xs: x/p update (read x, p, r, dd; write x, p) + next SpMM (write q; CSR);
+        # the p rows it gathers were just written and are not re-read from DRAM
+        algo = {"k_xs": 48 * n * kp + 12 * nnz + 4 * (n + 1) + 16 * n,
+                "k_update_r": 24 * n * kp + 16 * n}
+        times = dict(zip(algo, [float(ms[0]), float(ms[1])]))
+    else:
+        algo = {"k_spmm_pq": 16 * n * kp + 12 * nnz + 4 * (n + 1),
+                "k_update_r": 24 * n * kp + 16 * n,
+                "k_update_xp": 40 * n * kp + 16 * n}
+        times = dict(zip(algo, [float(ms[0]), float(ms[1]), float(ms[2])]))
     peak, peak_kind = peaks()
     kern = {name: {"ms": times[name], "bytes": algo[name],
                    "gbs": algo[name] / (times[name] * 1e-3) / 1e9} for name in algo}
@@ -165,7 +173,8 @@ def kernel_roofline(engine, A, rounds=20):
             "traffic": traffic, "algorithmic_bytes_per_launch": algo[dominant],
             "launch_ms": round(times[dominant], 4),
             "share_of_round": round(times[dominant] / total_ms, 3),
-            "pcg_round": {"kp": kp, "n": n, "nnz_spmm": nnz, "ms": round(total_ms, 4),
+            "pcg_round": {"kp": kp, "n": n, "nnz_spmm": nnz, "fused": bool(fused.value),
+                          "ms": round(total_ms, 4),
                           "bytes": total_bytes,
                           "gbs": round(total_bytes / (total_ms * 1e-3) / 1e9, 1),
                           "frac": round(total_bytes / (total_ms * 1e-3) / 1e9 / peak, 4),

@@ -27,6 +27,8 @@
 // Reductions are deterministic: fixed row->block mapping, fixed in-block tree,
 // and the last block to finish sums the per-block partials in block order.
 #include <math.h>
+
+#include <algorithm>
 #include <stdlib.h>
 #include <string.h>
 
@@ -55,6 +57,8 @@ enum : int { SUM_RUN = 0, SUM_CHECK = 1, SUM_REPLACE = 2, SUM_MASKED = 3, SUM_N 
 
 struct Ctl {
   int n, kp, G;
+  int nb, tpb, delta;  // k_xs band schedule: bands, tiles per block per band, band reach
+  int* xdone;          // k_xs: blocks done with each band's x/p update
   double tol;
   int max_iter;
   double *normb, *rz, *alpha, *beta, *best_res, *true_res;
@@ -380,200 +384,205 @@ __device__ __forceinline__ void gather_rows(const Csr& A, const double* __restri
   }
 }
 
-// Whole-block sweep over this block's rows: calls epi(row[R], acc[R][CPL]).
-// For row groups of >= 16 lanes the CSR stream is software-pipelined in
-// registers: step s gathers with the (index, value) pairs loaded during step
-// s-1 while the pairs of step s+1 and the row pointers of step s+2 are in
-// flight, so a row costs one memory latency instead of three dependent ones
-// (indptr -> indices -> gathered rows).  Lane g of a row group holds the
-// row's entry g; rows with more entries than lanes finish with direct loads.
-template <int KP, int R>
-__device__ __forceinline__ void load_meta(const Ctl& c, const Csr& A, int t0, int nt,
-                                          int (&row)[R], int (&st)[R], int (&ln)[R]) {
+// Tile schedules: slot s of a block -> tile index (>= the tile count: idle).
+struct LinearSched {  // tiles blockIdx.x + s*G (the whole grid sweeps one band)
+  int G;
+  __device__ __forceinline__ int tile(int s) const { return blockIdx.x + s * G; }
+};
+struct BandSched {  // band-major: band b holds G*tpb tiles, tpb per block (k_xs)
+  int G, tpb;
+  __device__ __forceinline__ int tile(int s) const {
+    return (s / tpb) * G * tpb + blockIdx.x + G * (s % tpb);
+  }
+};
+struct NoHook {
+  __device__ __forceinline__ void operator()(int) const {}
+};
+
+template <int KP>
+__device__ __forceinline__ void load_meta(const Ctl& c, const Csr& A, int tile, int nt, int& row,
+                                          int& st, int& ln) {
   using M = Map<KP>;
-  const int gl = threadIdx.x / M::LPR;
+  const int rw = tile * M::RB + threadIdx.x / M::LPR;
+  row = (tile < nt && rw < c.n) ? rw : -1;
+  st = 0;
+  ln = 0;
+  if (row >= 0) {
+    st = __ldg(A.indptr + row);
+    ln = __ldg(A.indptr + row + 1) - st;
+  }
+}
+
+template <int KP>
+__device__ __forceinline__ void load_entries(const Csr& A, int st, int ln,
+                                             int (&ci)[Spmm<KP>::EPL],
+                                             double (&cv)[Spmm<KP>::EPL]) {
+  constexpr int LPR = Map<KP>::LPR;
+  const int glane = threadIdx.x % LPR;
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int t = t0 + r * c.G;
-    const int rw = t * M::RB + gl;
-    row[r] = (t < nt && rw < c.n) ? rw : -1;
-    st[r] = 0;
-    ln[r] = 0;
-    if (row[r] >= 0) {
-      st[r] = __ldg(A.indptr + row[r]);
-      ln[r] = __ldg(A.indptr + row[r] + 1) - st[r];
+  for (int q = 0; q < Spmm<KP>::EPL; ++q) {
+    const int e = q * LPR + glane;
+    ci[q] = 0;
+    cv[q] = 0.0;
+    if (e < ln) {
+      ci[q] = __ldg(A.indices + st + e);
+      cv[q] = __ldg(A.val + st + e);
     }
   }
 }
 
-template <int KP, int R>
-__device__ __forceinline__ void load_entries(const Csr& A, const int (&st)[R], const int (&ln)[R],
-                                             int (&ci)[R][Spmm<KP>::EPL],
-                                             double (&cv)[R][Spmm<KP>::EPL]) {
-  constexpr int LPR = Map<KP>::LPR;
-  const int glane = threadIdx.x % LPR;
-#pragma unroll
-  for (int r = 0; r < R; ++r)
-#pragma unroll
-    for (int q = 0; q < Spmm<KP>::EPL; ++q) {
-      const int e = q * LPR + glane;
-      ci[r][q] = 0;
-      cv[r][q] = 0.0;
-      if (e < ln[r]) {
-        ci[r][q] = __ldg(A.indices + st[r] + e);
-        cv[r][q] = __ldg(A.val + st[r] + e);
-      }
-    }
+template <int CPL, bool NC>
+__device__ __forceinline__ void gather_cols(const double* p, double (&v)[CPL]) {
+  if constexpr (NC)
+    ldg_cols<CPL>(p, v);
+  else
+    ld_cols<CPL>(p, v);  // coherent: V is written inside the same launch (k_xs)
 }
 
-template <int KP, class Epi>
-__device__ __forceinline__ void spmm_sweep(const Ctl& c, const Csr& A, const double* __restrict__ V,
-                                           bool any, Epi&& epi) {
+// Sweep over a block's slots: calls hook(s) at the top of slot s, then
+// epi(row, acc) with acc = sum_j a_ij V[col_j, lane columns] for the slot's row
+// (row < 0: idle).  For row groups of >= 8 lanes the CSR stream is
+// software-pipelined in registers: row pointers 3 slots ahead, (index, value)
+// pairs 2 slots ahead (lane g of a row group holds entries g, g+LPR, ...), an
+// L2 bulk prefetch of each row's largest-index neighbour 1 slot ahead (on a
+// grid-ordered mesh the +z neighbour, the row the sweep touches first, i.e.
+// the DRAM miss), and the current slot's gathers issued GB at a time before
+// any FMA consumes them.  So a row costs one memory latency instead of three
+// dependent ones (indptr -> indices -> gathered rows).
+template <int KP, bool NC, class Sched, class Hook, class Epi>
+__device__ __forceinline__ void spmm_slots(const Ctl& c, const Csr& A, const double* V, bool any,
+                                           int nslots, const Sched& sc, Hook&& hook, Epi&& epi) {
   using M = Map<KP>;
-  constexpr int R = Spmm<KP>::R, LPR = M::LPR, CPL = M::CPL, EPL = Spmm<KP>::EPL;
+  static_assert(Spmm<KP>::R == 1, "one row per row group per slot");
+  constexpr int LPR = M::LPR, CPL = M::CPL, EPL = Spmm<KP>::EPL;
   constexpr int CAP = LPR * EPL;  // entries per row served from registers
   const int nt = n_tiles(c.n, M::RB);
-  const int step = R * c.G;
+  const int glane = threadIdx.x % LPR;
+  const double* Vl = V + glane * CPL;
+  auto tile_of = [&](int s) { return s < nslots ? sc.tile(s) : nt; };
   if constexpr (!Spmm<KP>::PIPELINED) {
-    const int gl = threadIdx.x / LPR;
-    for (int t0 = blockIdx.x; t0 < nt; t0 += step) {
-      int row[R];
-#pragma unroll
-      for (int r = 0; r < R; ++r) {
-        const int t = t0 + r * c.G;
-        row[r] = (t < nt && t * M::RB + gl < c.n) ? t * M::RB + gl : -1;
-      }
-      double acc[R][CPL];
-      gather_rows<KP, R>(A, V, row, any, acc);
-      epi(row, acc);
+    for (int s = 0; s < nslots; ++s) {
+      hook(s);
+      int row[1];
+      const int t = tile_of(s);
+      const int rw = t * M::RB + threadIdx.x / LPR;
+      row[0] = (t < nt && rw < c.n) ? rw : -1;
+      double acc[1][CPL];
+      gather_rows<KP, 1>(A, V, row, any, acc);
+      epi(row[0], acc[0]);
     }
   } else {
-    const int glane = threadIdx.x % LPR;
-    const double* __restrict__ Vl = V + glane * CPL;
-    // pipeline: row pointers 3 steps ahead, (index, value) pairs 2 steps
-    // ahead, and one step ahead an L2 bulk prefetch of each row's largest-index
-    // neighbour (on a grid-ordered mesh the +z neighbour: the row this sweep
-    // touches first, i.e. the DRAM miss), then the gathers of the current step.
-    int row[R], st[R], ln[R], ci[R][EPL];
-    double cv[R][EPL];
-    int rowN[R], stN[R], lnN[R], ciN[R][EPL];
-    double cvN[R][EPL];
-    int rowNN[R], stNN[R], lnNN[R];
-    int t0 = blockIdx.x;
-    load_meta<KP, R>(c, A, t0, nt, row, st, ln);
-    load_entries<KP, R>(A, st, ln, ci, cv);
-    load_meta<KP, R>(c, A, t0 + step, nt, rowN, stN, lnN);
-    load_entries<KP, R>(A, stN, lnN, ciN, cvN);
-    load_meta<KP, R>(c, A, t0 + 2 * step, nt, rowNN, stNN, lnNN);
-    for (; t0 < nt; t0 += step) {
-      int ciNN[R][EPL], rowN3[R], stN3[R], lnN3[R];
-      double cvNN[R][EPL];
-      load_entries<KP, R>(A, stNN, lnNN, ciNN, cvNN);               // step s+2 pairs
-      load_meta<KP, R>(c, A, t0 + 3 * step, nt, rowN3, stN3, lnN3);  // step s+3 pointers
+    int row, st, ln, ci[EPL];
+    double cv[EPL];
+    int rowN, stN, lnN, ciN[EPL];
+    double cvN[EPL];
+    int rowNN, stNN, lnNN;
+    load_meta<KP>(c, A, tile_of(0), nt, row, st, ln);
+    load_entries<KP>(A, st, ln, ci, cv);
+    load_meta<KP>(c, A, tile_of(1), nt, rowN, stN, lnN);
+    load_entries<KP>(A, stN, lnN, ciN, cvN);
+    load_meta<KP>(c, A, tile_of(2), nt, rowNN, stNN, lnNN);
+    for (int s = 0; s < nslots; ++s) {
+      int ciNN[EPL], rowN3, stN3, lnN3;
+      double cvNN[EPL];
+      load_entries<KP>(A, stNN, lnNN, ciNN, cvNN);             // slot s+2 pairs
+      load_meta<KP>(c, A, tile_of(s + 3), nt, rowN3, stN3, lnN3);  // slot s+3 pointers
+      hook(s);
       if (any) {
-#pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int e = lnN[r] - 1;  // sorted columns: the last entry is the largest index
-          if (e >= 0 && e < CAP && glane == e % LPR) {
-            const int cc = (e / LPR == 0) ? ciN[r][0] : ciN[r][EPL - 1];
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(V + (size_t)cc * KP),
-                         "r"(KP * 8)
-                         : "memory");
-          }
+        const int e = lnN - 1;  // sorted columns: the last entry is the largest index
+        if (e >= 0 && e < CAP && glane == e % LPR) {
+          const int cc = (e / LPR == 0) ? ciN[0] : ciN[EPL - 1];
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(V + (size_t)cc * KP),
+                       "r"(KP * 8)
+                       : "memory");
         }
       }
-      double acc[R][CPL];
-      int maxlen = 0;
+      double acc[CPL];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-#pragma unroll
-        for (int k = 0; k < CPL; ++k) acc[r][k] = 0.0;
-        maxlen = max(maxlen, ln[r]);
-      }
+      for (int k = 0; k < CPL; ++k) acc[k] = 0.0;
+      int maxlen = ln;
       if (LPR < 32) maxlen = (int)__reduce_max_sync(FULL, (unsigned)maxlen);
-      int lim[R];  // entries this lane group gathers from registers (0 if no active column)
-#pragma unroll
-      for (int r = 0; r < R; ++r) lim[r] = any ? min(ln[r], CAP) : 0;
+      const int lim = any ? min(ln, CAP) : 0;  // entries gathered from registers
       const int inreg = min(maxlen, CAP);
-      // batches of GB entries: all GB gathers issued before the FMAs use them
 #pragma unroll
       for (int q = 0; q < EPL; ++q) {
         if (q * LPR >= inreg) break;
 #pragma unroll
         for (int b = 0; b < LPR; b += GB) {
           if (q * LPR + b >= inreg) break;
-          double g[R][GB][CPL];
+          double g[GB][CPL];
 #pragma unroll
-          for (int r = 0; r < R; ++r)
+          for (int t = 0; t < GB; ++t) {
+            const int e = q * LPR + b + t;
+            const int cc = __shfl_sync(FULL, ci[q], (b + t) % LPR, LPR);
+            if (e < lim) gather_cols<CPL, NC>(Vl + (size_t)cc * KP, g[t]);
+          }
 #pragma unroll
-            for (int t = 0; t < GB; ++t) {
-              const int e = q * LPR + b + t;
-              const int cc = __shfl_sync(FULL, ci[r][q], (b + t) % LPR, LPR);
-              if (e < lim[r]) ldg_cols<CPL>(Vl + (size_t)cc * KP, g[r][t]);
+          for (int t = 0; t < GB; ++t) {
+            const int e = q * LPR + b + t;
+            const double vv = __shfl_sync(FULL, cv[q], (b + t) % LPR, LPR);
+            if (e < lim) {
+#pragma unroll
+              for (int k = 0; k < CPL; ++k) acc[k] = fma(vv, g[t][k], acc[k]);
             }
-#pragma unroll
-          for (int r = 0; r < R; ++r)
-#pragma unroll
-            for (int t = 0; t < GB; ++t) {
-              const int e = q * LPR + b + t;
-              const double vv = __shfl_sync(FULL, cv[r][q], (b + t) % LPR, LPR);
-              if (e < lim[r]) {
-#pragma unroll
-                for (int k = 0; k < CPL; ++k) acc[r][k] = fma(vv, g[r][t][k], acc[r][k]);
-              }
-            }
+          }
         }
       }
       if (maxlen > CAP) {  // long rows: remaining entries straight from memory
+        for (int e = CAP; e < ln; ++e) {
+          const int cc = __ldg(A.indices + st + e);
+          const double vv = __ldg(A.val + st + e);
+          if (any) {
+            double g[CPL];
+            gather_cols<CPL, NC>(Vl + (size_t)cc * KP, g);
 #pragma unroll
-        for (int r = 0; r < R; ++r)
-          for (int e = CAP; e < ln[r]; ++e) {
-            const int cc = __ldg(A.indices + st[r] + e);
-            const double vv = __ldg(A.val + st[r] + e);
-            if (any) {
-              double g[CPL];
-              ldg_cols<CPL>(Vl + (size_t)cc * KP, g);
-#pragma unroll
-              for (int k = 0; k < CPL; ++k) acc[r][k] = fma(vv, g[k], acc[r][k]);
-            }
+            for (int k = 0; k < CPL; ++k) acc[k] = fma(vv, g[k], acc[k]);
           }
+        }
       }
       epi(row, acc);
+      row = rowN;
+      st = stN;
+      ln = lnN;
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        row[r] = rowN[r];
-        st[r] = stN[r];
-        ln[r] = lnN[r];
-#pragma unroll
-        for (int q = 0; q < EPL; ++q) {
-          ci[r][q] = ciN[r][q];
-          cv[r][q] = cvN[r][q];
-          ciN[r][q] = ciNN[r][q];
-          cvN[r][q] = cvNN[r][q];
-        }
-        rowN[r] = rowNN[r];
-        stN[r] = stNN[r];
-        lnN[r] = lnNN[r];
-        rowNN[r] = rowN3[r];
-        stNN[r] = stN3[r];
-        lnNN[r] = lnN3[r];
+      for (int q = 0; q < EPL; ++q) {
+        ci[q] = ciN[q];
+        cv[q] = cvN[q];
+        ciN[q] = ciNN[q];
+        cvN[q] = cvNN[q];
       }
+      rowN = rowNN;
+      stN = stNN;
+      lnN = lnNN;
+      rowNN = rowN3;
+      stNN = stN3;
+      lnNN = lnN3;
     }
   }
+}
+
+template <int KP, class Epi>
+__device__ __forceinline__ void spmm_sweep(const Ctl& c, const Csr& A, const double* __restrict__ V,
+                                           bool any, Epi&& epi) {
+  const int nt = n_tiles(c.n, Map<KP>::RB);
+  const int nslots = (nt - (int)blockIdx.x + c.G - 1) / c.G;
+  spmm_slots<KP, true>(c, A, V, any, nslots, LinearSched{c.G}, NoHook{}, epi);
 }
 
 // q = A p, partial p.q, alpha = rz / p.q       (solver.py:87-88)
 template <int KP>
 __global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
-    k_spmm_pq(Ctl c, Csr A, const double* __restrict__ P, double* __restrict__ Q) {
+    k_spmm_pq(Ctl c, Csr A, const double* __restrict__ P, double* __restrict__ Q, int mode) {
+  // mode 0: every RUN column; mode 1: the columns the check path just resumed
+  // (pmask), so that q = A p exists for them before the next k_update_r.
   using M = Map<KP>;
-  constexpr int R = Spmm<KP>::R;
   __shared__ double sm[M::RED];
   __shared__ double tot[KP];
   __shared__ int s_act[KP];
-  if (c.summary[SUM_RUN] == 0) return;
-  const int tid = threadIdx.x, gl = tid / M::LPR, glane = tid % M::LPR;
-  for (int j = tid; j < KP; j += BLOCK) s_act[j] = (c.state[j] == S_RUN);
+  if (c.summary[mode == 0 ? SUM_RUN : SUM_REPLACE] == 0) return;
+  const int tid = threadIdx.x, glane = tid % M::LPR;
+  for (int j = tid; j < KP; j += BLOCK)
+    s_act[j] = (mode == 0) ? (c.state[j] == S_RUN) : (c.pmask[j] != 0);
   __syncthreads();
   bool act[M::CPL];
   bool any = false;
@@ -586,24 +595,20 @@ __global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
   double v[1][M::CPL];
 #pragma unroll
   for (int k = 0; k < M::CPL; ++k) v[0][k] = 0.0;
-  spmm_sweep<KP>(c, A, P, any, [&](const int (&row)[R], double (&acc)[R][M::CPL]) {
-    if (!any) return;
+  spmm_sweep<KP>(c, A, P, any, [&](int row, double (&acc)[M::CPL]) {
+    if (!any || row < 0) return;
+    const size_t o = (size_t)row * KP + glane * M::CPL;
+    st_cols<M::CPL>(Q + o, acc);
+    double p[M::CPL];
+    ldg_cols<M::CPL>(P + o, p);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (row[r] < 0) continue;
-      const size_t o = (size_t)row[r] * KP + glane * M::CPL;
-      st_cols<M::CPL>(Q + o, acc[r]);
-      double p[M::CPL];
-      ldg_cols<M::CPL>(P + o, p);
-#pragma unroll
-      for (int k = 0; k < M::CPL; ++k)
-        if (act[k]) v[0][k] += p[k] * acc[r][k];
-    }
+    for (int k = 0; k < M::CPL; ++k)
+      if (act[k]) v[0][k] += p[k] * acc[k];
   });
   block_partials<KP, 1>(v, sm, c.part0, nullptr);
   if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
   if (tid < KP) {
-    if (c.state[tid] == S_RUN) c.alpha[tid] = c.rz[tid] / tot[tid];
+    if (s_act[tid]) c.alpha[tid] = c.rz[tid] / tot[tid];
   }
 }
 
@@ -779,6 +784,117 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
   }
 }
 
+// ---------------------------------------------------------------- fused x/p update + SpMM
+// One launch does round k's  x += alpha p, p = r/d + beta p  and round k+1's
+// q = A p, p.q.  Rows are grouped in bands of G*tpb tiles.  Every block first
+// updates its tiles of band b (k_update_xp's arithmetic), publishes that on
+// xdone[b], and gathers for band j only after all blocks have published every
+// band j' <= j + delta (delta bands cover the matrix bandwidth).  The p rows
+// the SpMM gathers were therefore written moments earlier and are still in
+// L2: the SpMM's DRAM read of P disappears and the launch count per round
+// drops from 3 to 2.  Per-column arithmetic and every reduction order equal
+// the three-kernel path (same tiles per block, same in-block trees).
+// Requires all G blocks co-resident: launched cooperatively.
+template <int KP>
+__global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
+    k_xs(Ctl c, Csr A, double* X, double* P, const double* __restrict__ R, double* Q) {
+  using M = Map<KP>;
+  __shared__ double sm[M::RED];
+  __shared__ double tot[KP];
+  __shared__ double s_alpha[KP], s_beta[KP];
+  __shared__ int s_xm[KP], s_pm[KP];
+  if (c.summary[SUM_MASKED] == 0) return;  // uniform: every block returns
+  const int tid = threadIdx.x, gl = tid / M::LPR, glane = tid % M::LPR;
+  for (int j = tid; j < KP; j += BLOCK) {
+    s_xm[j] = c.xmask[j];
+    s_pm[j] = c.pmask[j];
+    s_alpha[j] = c.alpha[j];
+    s_beta[j] = c.beta[j];
+  }
+  __syncthreads();
+  // per-column factors stay in shared memory (registers are the SpMM's)
+  const int j0 = glane * M::CPL;
+  bool anyx = false, anyp = false;
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) {
+    anyx |= s_xm[j0 + k] != 0;
+    anyp |= s_pm[j0 + k] != 0;
+  }
+  const int nt = n_tiles(c.n, M::RB);
+  const BandSched sc{c.G, c.tpb};
+  // x/p update of this block's tiles of band b, then publish it
+  auto xphase = [&](int b) {
+    if (anyx || anyp) {
+      for (int i = 0; i < c.tpb; ++i) {
+        const int t = sc.tile(b * c.tpb + i);
+        const int row = t * M::RB + gl;
+        if (t >= nt || row >= c.n) continue;
+        const size_t o = (size_t)row * KP + glane * M::CPL;
+        double p[M::CPL], x[M::CPL], r[M::CPL];
+        double2 dd;
+        ld_cols<M::CPL>(P + o, p);
+        if (anyx) ld_cols<M::CPL>(X + o, x);
+        if (anyp) {
+          ld_cols<M::CPL>(R + o, r);
+          dd = c.dd[row];
+        }
+        if (anyx) {
+#pragma unroll
+          for (int k = 0; k < M::CPL; ++k)
+            if (s_xm[j0 + k]) x[k] = x[k] + s_alpha[j0 + k] * p[k];
+          st_cols<M::CPL>(X + o, x);
+        }
+        if (anyp) {
+#pragma unroll
+          for (int k = 0; k < M::CPL; ++k)
+            if (s_pm[j0 + k]) p[k] = zdiv(r[k], dd) + s_beta[j0 + k] * p[k];
+          st_cols<M::CPL>(P + o, p);
+        }
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) atomicAdd(c.xdone + b, 1);
+  };
+  auto wait_band = [&](int b) {
+    if (tid == 0) {
+      const volatile int* f = c.xdone + b;
+      while (*f < c.G) __nanosleep(64);
+      __threadfence();
+    }
+    __syncthreads();
+  };
+  const int nb = c.nb, dl = c.delta;
+  for (int b = 0; b <= dl && b < nb; ++b) xphase(b);
+  int xnext = dl + 1;  // next band this block updates
+  auto hook = [&](int s) {
+    if (s % c.tpb) return;
+    const int j = s / c.tpb;  // band whose rows this slot starts
+    if (xnext < nb && xnext <= j + dl + 1) xphase(xnext++);
+    wait_band(min(j + dl, nb - 1));
+  };
+  double v[1][M::CPL];
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) v[0][k] = 0.0;
+  spmm_slots<KP, false>(c, A, P, anyp, nb * c.tpb, sc, hook, [&](int row, double (&acc)[M::CPL]) {
+    if (!anyp || row < 0) return;
+    const size_t o = (size_t)row * KP + glane * M::CPL;
+    st_cols<M::CPL>(Q + o, acc);
+    double p[M::CPL];
+    ld_cols<M::CPL>(P + o, p);
+#pragma unroll
+    for (int k = 0; k < M::CPL; ++k)
+      if (s_pm[j0 + k]) v[0][k] += p[k] * acc[k];
+  });
+  while (xnext < nb) xphase(xnext++);  // (only when the slot loop ended early)
+  block_partials<KP, 1>(v, sm, c.part0, nullptr);
+  if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
+  if (tid < KP) {
+    if (s_pm[tid]) c.alpha[tid] = c.rz[tid] / tot[tid];
+  }
+  for (int b = tid; b < nb; b += BLOCK) c.xdone[b] = 0;  // every block has left its waits
+}
+
 // ---------------------------------------------------------------- check path
 // s = b - A x for CHECK columns (into Q), true residual, DONE / FAILED / REPLACE
 // (solver.py:94-102)
@@ -787,7 +903,6 @@ __global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
     k_spmm_resid(Ctl c, Csr A, const double* __restrict__ B, const double* __restrict__ X,
                  double* __restrict__ Q) {
   using M = Map<KP>;
-  constexpr int R = Spmm<KP>::R;
   __shared__ double sm[M::RED];
   __shared__ double tot[KP];
   __shared__ int s_act[KP];
@@ -795,7 +910,7 @@ __global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
     if (blockIdx.x == 0 && threadIdx.x == 0) c.summary[SUM_REPLACE] = 0;
     return;
   }
-  const int tid = threadIdx.x, gl = tid / M::LPR, glane = tid % M::LPR;
+  const int tid = threadIdx.x, glane = tid % M::LPR;
   for (int j = tid; j < KP; j += BLOCK) s_act[j] = (c.state[j] == S_CHECK);
   __syncthreads();
   bool act[M::CPL];
@@ -809,23 +924,19 @@ __global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
   double v[1][M::CPL];
 #pragma unroll
   for (int k = 0; k < M::CPL; ++k) v[0][k] = 0.0;
-  spmm_sweep<KP>(c, A, X, any, [&](const int (&row)[R], double (&acc)[R][M::CPL]) {
-    if (!any) return;
+  spmm_sweep<KP>(c, A, X, any, [&](int row, double (&acc)[M::CPL]) {
+    if (!any || row < 0) return;
+    const size_t o = (size_t)row * KP + glane * M::CPL;
+    double b[M::CPL], q[M::CPL];
+    ld_cols<M::CPL>(B + o, b);
+    ld_cols<M::CPL>(Q + o, q);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (row[r] < 0) continue;
-      const size_t o = (size_t)row[r] * KP + glane * M::CPL;
-      double b[M::CPL], q[M::CPL];
-      ld_cols<M::CPL>(B + o, b);
-      ld_cols<M::CPL>(Q + o, q);
-#pragma unroll
-      for (int k = 0; k < M::CPL; ++k)
-        if (act[k]) {
-          q[k] = b[k] - acc[r][k];
-          v[0][k] += q[k] * q[k];
-        }
-      st_cols<M::CPL>(Q + o, q);
-    }
+    for (int k = 0; k < M::CPL; ++k)
+      if (act[k]) {
+        q[k] = b[k] - acc[k];
+        v[0][k] += q[k] * q[k];
+      }
+    st_cols<M::CPL>(Q + o, q);
   });
   block_partials<KP, 1>(v, sm, c.part0, nullptr);
   if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
@@ -929,6 +1040,8 @@ struct Layout {
   int *iters, *best_iter, *state, *xmask, *pmask, *freeze;
   unsigned int* counter;
   int* summary;
+  int* xdone;  // k_xs band counters (one per band; bands <= tiles)
+  int* bw;     // matrix bandwidth scratch
   size_t bytes;
 };
 
@@ -957,8 +1070,80 @@ inline Layout carve(void* ws, int n, int kp) {
   L.freeze = cv.take<int>(kp);
   L.counter = cv.take<unsigned int>(4);
   L.summary = cv.take<int>(SUM_N);
+  L.xdone = cv.take<int>((size_t)n + 2);
+  L.bw = cv.take<int>(2);
   L.bytes = cv.used + 256;
   return L;
+}
+
+__global__ void k_bandwidth(int n, const int32_t* __restrict__ indptr,
+                            const int32_t* __restrict__ indices, int* __restrict__ bw) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int s = indptr[i], e = indptr[i + 1];
+  if (s < e) atomicMax(bw, max(i - indices[s], indices[e - 1] - i));
+}
+
+// The fused x/p-update + SpMM round (k_xs) is correct but, with the SpMM's
+// 128-register budget, its streaming half runs at 16 warps/SM and loses to
+// the three-kernel round (1.28 vs 1.00 ms at C2, kp=64).  Opt in with
+// HFB200_FUSED=1 while it is being reworked (warp-specialised x/p warps).
+inline bool fused_enabled() {
+  const char* v = getenv("HFB200_FUSED");
+  return v && v[0] == '1';
+}
+
+// Control block and grids for one solve.  c: streaming kernels; cs: SpMM and
+// fused kernels (one block per SM for 4-column lanes) with the band schedule.
+template <int KP>
+int setup(const Layout& L, const hf_csr* A, int n, double tol, int max_iter, Ctl& c, Ctl& cs,
+          bool& fused, cudaStream_t stream) {
+  memset(&c, 0, sizeof(c));
+  c.n = n;
+  c.kp = KP;
+  c.G = grid_for(n, KP);
+  c.tol = tol;
+  c.max_iter = max_iter;
+  c.normb = L.normb; c.rz = L.rz; c.alpha = L.alpha; c.beta = L.beta;
+  c.best_res = L.best_res; c.true_res = L.true_res; c.iters = L.iters;
+  c.best_iter = L.best_iter; c.state = L.state; c.xmask = L.xmask; c.pmask = L.pmask;
+  c.freeze = nullptr; c.part0 = L.part0; c.part1 = L.part1; c.dd = L.dd;
+  c.counter = L.counter; c.summary = L.summary; c.xdone = L.xdone;
+  cs = c;
+  cs.G = grid_for(n, KP, Spmm<KP>::BPS);
+  fused = Spmm<KP>::PIPELINED && fused_enabled();
+  if (fused) {  // band schedule from the matrix bandwidth (max |col - row|)
+    HF_CUDA(cudaMemsetAsync(L.bw, 0, sizeof(int), stream));
+    k_bandwidth<<<(n + 255) / 256, 256, 0, stream>>>(n, A->indptr, A->indices, L.bw);
+    HF_LAUNCH_CHECK();
+    count_launches(1);
+    int bw = 0;
+    HF_CUDA(cudaMemcpyAsync(&bw, L.bw, sizeof(int), cudaMemcpyDeviceToHost, stream));
+    HF_CUDA(cudaStreamSynchronize(stream));
+    const long rows_per_tileset = (long)cs.G * Map<KP>::RB;
+    const int nt = n_tiles(n, Map<KP>::RB);
+    cs.tpb = (int)std::max<long>(1, (bw + rows_per_tileset - 1) / rows_per_tileset);
+    const long band_rows = rows_per_tileset * cs.tpb;
+    cs.delta = bw == 0 ? 0 : (int)((bw + band_rows - 1) / band_rows);
+    cs.nb = (int)((nt + (long)cs.G * cs.tpb - 1) / ((long)cs.G * cs.tpb));
+    HF_CUDA(cudaMemsetAsync(L.xdone, 0, sizeof(int) * (cs.nb + 1), stream));
+  }
+  return HF_OK;
+}
+
+template <int KP>
+cudaError_t launch_xs(const Ctl& cs, const Csr& csr, double* X, double* P, const double* R,
+                      double* Q, cudaStream_t s) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(cs.G);
+  cfg.blockDim = dim3(BLOCK);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;  // all blocks co-resident: band waits cannot deadlock
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_xs<KP>, cs, csr, X, P, R, Q);
 }
 
 template <int KP>
@@ -970,40 +1155,24 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
     set_error("pcg workspace too small: need %zu, have %zu", L.bytes, ws_bytes);
     return HF_ERR_WORKSPACE;
   }
-  Ctl c;
-  c.n = n;
-  c.kp = KP;
-  c.G = grid_for(n, KP);
-  c.tol = tol;
-  c.max_iter = max_iter;
-  c.normb = L.normb;
-  c.rz = L.rz;
-  c.alpha = L.alpha;
-  c.beta = L.beta;
-  c.best_res = L.best_res;
-  c.true_res = L.true_res;
-  c.iters = L.iters;
-  c.best_iter = L.best_iter;
-  c.state = L.state;
-  c.xmask = L.xmask;
-  c.pmask = L.pmask;
-  c.freeze = nullptr;
-  c.part0 = L.part0;
-  c.part1 = L.part1;
-  c.dd = L.dd;
-  c.counter = L.counter;
-  c.summary = L.summary;
+  Ctl c, cs;
+  bool fused = false;
+  Csr csr{A->indptr, A->indices, A->val};
+  if (int rc = setup<KP>(L, A, n, tol, max_iter, c, cs, fused, stream)) return rc;
   if (freeze_at != nullptr) {
     HF_CUDA(cudaMemcpyAsync(L.freeze, freeze_at, sizeof(int) * KP, cudaMemcpyDeviceToDevice, stream));
     c.freeze = L.freeze;
+    cs.freeze = L.freeze;
   }
-  Csr csr{A->indptr, A->indices, A->val};
-  Ctl cs = c;  // the SpMM kernels run their own grid (one block per SM)
-  cs.G = grid_for(n, KP, Spmm<KP>::BPS);
   HF_CUDA(cudaMemsetAsync(L.counter, 0, sizeof(unsigned int) * 4, stream));
   k_init<KP><<<c.G, BLOCK, 0, stream>>>(c, B, d, X, L.R, L.P);
   HF_LAUNCH_CHECK();
   count_launches(1);
+  if (fused) {  // q = A p of the first round; later rounds get it from k_xs
+    k_spmm_pq<KP><<<cs.G, BLOCK, 0, stream>>>(cs, csr, L.P, L.Q, 0);
+    HF_LAUNCH_CHECK();
+    count_launches(1);
+  }
 
   int* h_sum = nullptr;
   HF_CUDA(cudaHostAlloc(&h_sum, sizeof(int) * SUM_N, cudaHostAllocDefault));
@@ -1027,25 +1196,36 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
 
   if (h_sum[SUM_RUN] > 0) {
     // Capture one chunk: CHUNK rounds, then the check path, then the status copy.
+    // Unfused round: spmm_pq, update_r, update_xp.  Fused round: update_r,
+    // k_xs (= update_xp of this round + spmm_pq of the next).
     HF_CUDA(cudaStreamCreateWithFlags(&guard.cs, cudaStreamNonBlocking));
     HF_CUDA(cudaStreamBeginCapture(guard.cs, cudaStreamCaptureModeThreadLocal));
+    cudaError_t le = cudaSuccess;
     for (int r = 0; r < CHUNK; ++r) {
-      k_spmm_pq<KP><<<cs.G, BLOCK, 0, guard.cs>>>(cs, csr, L.P, L.Q);
-      k_update_r<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, L.Q, L.R);
-      k_update_xp<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, SUM_MASKED, X, L.P, L.R);
+      if (fused) {
+        k_update_r<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, L.Q, L.R);
+        cudaError_t e = launch_xs<KP>(cs, csr, X, L.P, L.R, L.Q, guard.cs);
+        if (e != cudaSuccess) le = e;
+      } else {
+        k_spmm_pq<KP><<<cs.G, BLOCK, 0, guard.cs>>>(cs, csr, L.P, L.Q, 0);
+        k_update_r<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, L.Q, L.R);
+        k_update_xp<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, SUM_MASKED, X, L.P, L.R);
+      }
     }
     k_spmm_resid<KP><<<cs.G, BLOCK, 0, guard.cs>>>(cs, csr, B, X, L.Q);
     k_replace<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, L.Q, L.R);
     k_update_xp<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, SUM_REPLACE, X, L.P, L.R);
+    if (fused) k_spmm_pq<KP><<<cs.G, BLOCK, 0, guard.cs>>>(cs, csr, L.P, L.Q, 1);
     cudaMemcpyAsync(h_sum, L.summary, sizeof(int) * SUM_N, cudaMemcpyDeviceToHost, guard.cs);
     cudaError_t ce = cudaStreamEndCapture(guard.cs, &guard.g);
-    if (ce != cudaSuccess) {
-      set_error("graph capture failed: %s", cudaGetErrorString(ce));
+    if (ce != cudaSuccess || le != cudaSuccess) {
+      set_error("graph capture failed: %s / %s", cudaGetErrorString(ce), cudaGetErrorString(le));
       return HF_ERR_CUDA;
     }
     HF_CUDA(cudaGraphInstantiate(&guard.ge, guard.g, 0));
     HF_CUDA(cudaEventCreateWithFlags(&guard.ev[0], cudaEventDisableTiming));
     HF_CUDA(cudaEventCreateWithFlags(&guard.ev[1], cudaEventDisableTiming));
+    const long per_chunk = fused ? 2 * CHUNK + 4 : 3 * CHUNK + 3;
     // Every chunk costs at least one iteration of some column (or finishes a
     // CHECK); bound the loop generously and report if control never settles.
     const long max_chunks = 4L * (max_iter / CHUNK + 2) + 64;
@@ -1053,7 +1233,7 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
     bool finished = false;
     for (; i < max_chunks; ++i) {
       HF_CUDA(cudaGraphLaunch(guard.ge, stream));
-      count_launches(3 * CHUNK + 3);
+      count_launches(per_chunk);
       HF_CUDA(cudaEventRecord(guard.ev[i & 1], stream));
       if (i >= 1) {
         HF_CUDA(cudaEventSynchronize(guard.ev[(i - 1) & 1]));
@@ -1084,45 +1264,46 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
 }
 
 // Per-kernel timing of `rounds` PCG rounds with CUDA events on the launch
-// stream (bench.py roofline).  tol = 0 keeps every column running.
+// stream (bench.py roofline).  tol = 0 keeps every column running.  ms3 =
+// {k_spmm_pq, k_update_r, k_update_xp}, or {k_xs, k_update_r, 0} when fused.
 template <int KP>
 int profile(const hf_csr* A, const double* d, const double* B, int n, int rounds, double* X,
-            float* ms3, void* ws, size_t ws_bytes, cudaStream_t stream) {
+            float* ms3, int* fused_out, void* ws, size_t ws_bytes, cudaStream_t stream) {
   Layout L = carve(ws, n, KP);
   if (L.bytes > ws_bytes) {
     set_error("pcg workspace too small");
     return HF_ERR_WORKSPACE;
   }
-  Ctl c;
-  memset(&c, 0, sizeof(c));
-  c.n = n;
-  c.kp = KP;
-  c.G = grid_for(n, KP);
-  c.tol = 0.0;
-  c.max_iter = 1 << 30;
-  c.normb = L.normb; c.rz = L.rz; c.alpha = L.alpha; c.beta = L.beta;
-  c.best_res = L.best_res; c.true_res = L.true_res; c.iters = L.iters;
-  c.best_iter = L.best_iter; c.state = L.state; c.xmask = L.xmask; c.pmask = L.pmask;
-  c.freeze = nullptr; c.part0 = L.part0; c.part1 = L.part1; c.dd = L.dd; c.counter = L.counter;
-  c.summary = L.summary;
+  Ctl c, cs;
+  bool fused = false;
   Csr csr{A->indptr, A->indices, A->val};
-  Ctl cs = c;  // the SpMM kernels run their own grid (one block per SM)
-  cs.G = grid_for(n, KP, Spmm<KP>::BPS);
+  if (int rc = setup<KP>(L, A, n, 0.0, 1 << 30, c, cs, fused, stream)) return rc;
+  *fused_out = fused ? 1 : 0;
   HF_CUDA(cudaMemsetAsync(L.counter, 0, sizeof(unsigned int) * 4, stream));
   k_init<KP><<<c.G, BLOCK, 0, stream>>>(c, B, d, X, L.R, L.P);
+  if (fused) k_spmm_pq<KP><<<cs.G, BLOCK, 0, stream>>>(cs, csr, L.P, L.Q, 0);
   HF_LAUNCH_CHECK();
-  count_launches(1 + 3L * rounds);
+  count_launches((fused ? 2 : 1) + (fused ? 2L : 3L) * rounds);
   cudaEvent_t ev[4];
   for (auto& e : ev) HF_CUDA(cudaEventCreate(&e));
   double acc[3] = {0, 0, 0};
   for (int r = 0; r < rounds; ++r) {
-    cudaEventRecord(ev[0], stream);
-    k_spmm_pq<KP><<<cs.G, BLOCK, 0, stream>>>(cs, csr, L.P, L.Q);
-    cudaEventRecord(ev[1], stream);
-    k_update_r<KP><<<c.G, BLOCK, 0, stream>>>(c, L.Q, L.R);
-    cudaEventRecord(ev[2], stream);
-    k_update_xp<KP><<<c.G, BLOCK, 0, stream>>>(c, SUM_MASKED, X, L.P, L.R);
-    cudaEventRecord(ev[3], stream);
+    if (fused) {
+      cudaEventRecord(ev[0], stream);
+      HF_CUDA(launch_xs<KP>(cs, csr, X, L.P, L.R, L.Q, stream));
+      cudaEventRecord(ev[1], stream);
+      k_update_r<KP><<<c.G, BLOCK, 0, stream>>>(c, L.Q, L.R);
+      cudaEventRecord(ev[2], stream);
+      cudaEventRecord(ev[3], stream);
+    } else {
+      cudaEventRecord(ev[0], stream);
+      k_spmm_pq<KP><<<cs.G, BLOCK, 0, stream>>>(cs, csr, L.P, L.Q, 0);
+      cudaEventRecord(ev[1], stream);
+      k_update_r<KP><<<c.G, BLOCK, 0, stream>>>(c, L.Q, L.R);
+      cudaEventRecord(ev[2], stream);
+      k_update_xp<KP><<<c.G, BLOCK, 0, stream>>>(c, SUM_MASKED, X, L.P, L.R);
+      cudaEventRecord(ev[3], stream);
+    }
     HF_CUDA(cudaEventSynchronize(ev[3]));
     for (int k = 0; k < 3; ++k) {
       float t = 0.f;
@@ -1222,21 +1403,21 @@ extern "C" int hf_pcg_multi(const hf_csr* A, const double* d, const double* B, i
 }
 
 extern "C" int hf_pcg_profile(const hf_csr* A, const double* d, const double* B, int32_t n,
-                              int32_t kp, int32_t rounds, double* X, float* ms3, void* ws,
-                              size_t ws_bytes, void* stream) {
-  if (!A || !d || !B || !X || !ms3 || !ws || n <= 0 || rounds < 1) {
+                              int32_t kp, int32_t rounds, double* X, float* ms3, int32_t* fused,
+                              void* ws, size_t ws_bytes, void* stream) {
+  if (!A || !d || !B || !X || !ms3 || !fused || !ws || n <= 0 || rounds < 1) {
     set_error("hf_pcg_profile: bad argument");
     return HF_ERR_ARG;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   switch (kp) {
-    case 2: return pcg::profile<2>(A, d, B, n, rounds, X, ms3, ws, ws_bytes, s);
-    case 4: return pcg::profile<4>(A, d, B, n, rounds, X, ms3, ws, ws_bytes, s);
-    case 8: return pcg::profile<8>(A, d, B, n, rounds, X, ms3, ws, ws_bytes, s);
-    case 16: return pcg::profile<16>(A, d, B, n, rounds, X, ms3, ws, ws_bytes, s);
-    case 32: return pcg::profile<32>(A, d, B, n, rounds, X, ms3, ws, ws_bytes, s);
-    case 64: return pcg::profile<64>(A, d, B, n, rounds, X, ms3, ws, ws_bytes, s);
-    case 128: return pcg::profile<128>(A, d, B, n, rounds, X, ms3, ws, ws_bytes, s);
+    case 2: return pcg::profile<2>(A, d, B, n, rounds, X, ms3, fused, ws, ws_bytes, s);
+    case 4: return pcg::profile<4>(A, d, B, n, rounds, X, ms3, fused, ws, ws_bytes, s);
+    case 8: return pcg::profile<8>(A, d, B, n, rounds, X, ms3, fused, ws, ws_bytes, s);
+    case 16: return pcg::profile<16>(A, d, B, n, rounds, X, ms3, fused, ws, ws_bytes, s);
+    case 32: return pcg::profile<32>(A, d, B, n, rounds, X, ms3, fused, ws, ws_bytes, s);
+    case 64: return pcg::profile<64>(A, d, B, n, rounds, X, ms3, fused, ws, ws_bytes, s);
+    case 128: return pcg::profile<128>(A, d, B, n, rounds, X, ms3, fused, ws, ws_bytes, s);
     default:
       set_error("hf_pcg_profile: unsupported kp=%d", kp);
       return HF_ERR_ARG;
