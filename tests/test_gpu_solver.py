@@ -163,6 +163,21 @@ class TestTransferMatrix:
             assert np.linalg.norm(T[:, l] - x) / np.linalg.norm(x) < 1e-7
             assert np.linalg.norm(A @ T[:, l] - B[:, l]) / np.linalg.norm(B[:, l]) <= 1e-10
 
+    def test_fused_round_is_bit_identical(self, eng, monkeypatch):
+        """The fused x/p-update + SpMM round (HFB200_FUSED=1) reproduces the
+        three-kernel round bit for bit (same tiles per block, same trees)."""
+        from tests.fixtures import csr
+
+        fx = load("layered_h12.npz")
+        A = csr(fx, "A")
+        B = np.random.default_rng(5).normal(size=(A.shape[0], 40))
+        B[fx["ground"]] = 0.0
+        monkeypatch.setenv("HFB200_FUSED", "0")
+        T0 = eng.transfer_matrix(A, B)
+        monkeypatch.setenv("HFB200_FUSED", "1")
+        T1 = eng.transfer_matrix(A, B)
+        np.testing.assert_array_equal(T0, T1)
+
     def test_iterations_match_reference_per_column(self, eng):
         from paper_1811_07717_b200.solver import operator, rhs_block, solve_block
         from tests.fixtures import csr
