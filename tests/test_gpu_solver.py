@@ -90,6 +90,29 @@ class TestPcg:
         np.testing.assert_allclose(err.best_x, cases["fail30_best_x"], rtol=1e-10, atol=1e-14)
         assert err.column is None
 
+    def test_one_by_one(self, eng):
+        x, it, res = eng.pcg_solve(sp.csr_matrix(np.array([[2.0]])), np.array([4.0]))
+        np.testing.assert_allclose(x, [2.0], rtol=1e-15)
+        assert it == 1 and res == 0.0
+
+    def test_non_square_rejected(self, eng):
+        with pytest.raises(eng.ParameterError):
+            eng.pcg_solve(sp.csr_matrix(np.ones((3, 2))), np.ones(3))
+
+    def test_singular_preconditioner_only_with_nonzero_rhs(self, eng):
+        A = sp.csr_matrix(np.array([[1.0, 0.0], [0.0, 0.0]]))
+        x, it, _ = eng.pcg_solve(A, np.zeros(2))      # b = 0 returns before ldp (solver.py:75-77)
+        assert it == 0
+        with pytest.raises(eng.SingularPreconditionerError):
+            eng.pcg_solve(A, np.array([1.0, 0.0]))
+
+    @pytest.mark.parametrize("n,k", [(3, 130), (5, 64), (17, 33)])
+    def test_tiny_systems_many_columns(self, eng, n, k):
+        A = sp.csr_matrix(random_spd(n, seed=n, cond=10.0))
+        B = np.random.default_rng(k).normal(size=(n, k))
+        T = eng.transfer_matrix(A, B, eng.PcgConfig(tolerance=1e-12))
+        np.testing.assert_allclose(A @ T, B, rtol=0, atol=1e-10 * np.abs(B).max())
+
     def test_config_validation(self, eng):
         for kw in ({"tolerance": 0.0}, {"max_iterations": 0}, {"preconditioner": "amg"}):
             with pytest.raises(eng.ParameterError):
