@@ -135,7 +135,7 @@ def kernel_roofline(engine, A, rounds=20):
     k = min(kp, engine.Bd.shape[1])
     Bb[:, :k] = engine.Bd[:, :k]
     X = torch.empty_like(Bb)
-    ws = torch.empty(N.lib.hf_pcg_workspace_bytes(n, kp), dtype=torch.uint8, device=Bb.device)
+    ws = torch.empty(N.lib.hf_pcg_workspace_bytes(n, kp, op.Ac.nnz), dtype=torch.uint8, device=Bb.device)
     ms = (N.C.c_float * 3)()
     fused = N.C.c_int32(0)
     N.check("hf_pcg_profile", N.lib.hf_pcg_profile(

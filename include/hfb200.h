@@ -97,10 +97,11 @@ int hf_csr_prune_fill(const hf_csr* A, void* ws, size_t ws_bytes, int32_t* indpt
  *              replay a failed column to its best iterate.
  *   iters, status, best_iter  host, kp int32 each
  *   true_res, best_res        host, kp double each
+ * Workspace: hf_pcg_workspace_bytes(n, kp, A->nnz) bytes.
  * Result per column: status HF_COL_*; iters = converged iteration count;
  * true_res = ||b - A x|| / ||b|| at exit; best_res/best_iter = smallest
  * recurrence residual seen and the iteration it occurred at. */
-size_t hf_pcg_workspace_bytes(int32_t n, int32_t kp);
+size_t hf_pcg_workspace_bytes(int32_t n, int32_t kp, int64_t nnz);
 int hf_pcg_multi(const hf_csr* A, const double* d, const double* B, int32_t n, int32_t kp,
                  double tol, int32_t max_iter, const int32_t* freeze_at, double* X,
                  int32_t* iters, int32_t* status, double* true_res, double* best_res,

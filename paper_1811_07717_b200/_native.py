@@ -39,7 +39,7 @@ def _load():
         "hf_csr_prune_workspace_bytes": (SZ, [I32]),
         "hf_csr_prune_count": (C.c_int, [pcsr, P, SZ, C.POINTER(I64), P]),
         "hf_csr_prune_fill": (C.c_int, [pcsr, P, SZ, P, P, P, P]),
-        "hf_pcg_workspace_bytes": (SZ, [I32, I32]),
+        "hf_pcg_workspace_bytes": (SZ, [I32, I32, I64]),
         "hf_pcg_multi": (C.c_int, [pcsr, P, P, I32, I32, D, I32, P, P, P, P, P, P, P, P, SZ, P]),
         "hf_pcg_profile": (C.c_int, [pcsr, P, P, I32, I32, I32, P, P, C.POINTER(I32), P, SZ, P]),
         "hf_p1_blocks": (C.c_int, [P, P, I32, P, I32, P, I32, D, P, P, C.POINTER(I32), P]),

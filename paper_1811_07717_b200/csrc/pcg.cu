@@ -784,6 +784,315 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
   }
 }
 
+// ---------------------------------------------------------------- windowed SpMM (TMA)
+// On a grid-ordered mesh the rows one tile of TR consecutive rows gathers form
+// a handful of contiguous row ranges (x, y+-1, z+-1 neighbours).  A planner
+// (once per operator) records, per tile, those ranges (merged across gaps of
+// <= WGAP rows) and each entry's slot in the concatenated window.  The SpMM
+// then moves every window with one TMA bulk copy per range
+// (cp.async.bulk.shared::cluster.global) into shared memory, double-buffered
+// per half block on mbarriers, and reads the neighbour rows from shared
+// memory: no register-staged gathers, no L1 traffic, each neighbour row
+// fetched once per tile.  Tiles whose window does not fit (irregular meshes)
+// fall back to direct gathers.  The sums run over the same entries in the
+// same order as k_spmm_pq, so q is bitwise identical.
+constexpr int WIN_BYTES = 54 * 1024;  // shared-memory window per tile stage (108 rows at kp=64)
+constexpr int RCAP = 8;               // row ranges per window
+constexpr int WGAP = 2;               // ranges closer than this merge
+constexpr int WCAND = 512;            // columns per tile the planner handles
+constexpr int WHALF = BLOCK / 2;      // threads per tile (half block)
+
+template <int KP>
+struct Win {
+  static constexpr int TR = WHALF / Map<KP>::LPR;  // rows per tile
+  static constexpr int ROWB = KP * 8;              // bytes per P row
+  static constexpr int WROWS = WIN_BYTES / ROWB;   // window capacity (rows)
+  static constexpr int CAP = Map<KP>::LPR;         // entries per row held in registers
+};
+
+// tinfo[t] = {nranges (-1: fallback), slot of the tile's first row, window bytes, 0}
+__global__ void __launch_bounds__(256) k_plan_windows(int n, int tr, int wrows, int rowb,
+                                                      const int32_t* __restrict__ indptr,
+                                                      const int32_t* __restrict__ indices,
+                                                      int4* __restrict__ tinfo,
+                                                      int2* __restrict__ tranges,
+                                                      uint16_t* __restrict__ eslot) {
+  __shared__ int s_c[8][WCAND];
+  __shared__ int s_u[8][WCAND];
+  __shared__ short s_slot[8][WCAND];
+  __shared__ unsigned char s_f[8][WCAND];
+  __shared__ int s_ok[8];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t = blockIdx.x * 8 + warp;
+  const int ntile = (n + tr - 1) / tr;
+  if (t >= ntile) return;
+  const int r0 = t * tr, r1 = min(n, r0 + tr);
+  const int e0 = indptr[r0], E = indptr[r1] - e0;
+  if (E <= 0 || E > WCAND) {
+    if (lane == 0) tinfo[t] = make_int4(-1, 0, 0, 0);
+    return;
+  }
+  int* c = s_c[warp];
+  int* u = s_u[warp];
+  short* slot = s_slot[warp];
+  unsigned char* f = s_f[warp];
+  for (int i = lane; i < E; i += 32) c[i] = indices[e0 + i];
+  __syncwarp();
+  for (int i = lane; i < E; i += 32) {
+    bool first = true;
+    for (int j = 0; j < i; ++j)
+      if (c[j] == c[i]) {
+        first = false;
+        break;
+      }
+    f[i] = first;
+  }
+  __syncwarp();
+  int nu = 0;
+  for (int i = lane; i < E; i += 32) {
+    if (!f[i]) continue;
+    int rank = 0;
+    for (int j = 0; j < E; ++j) rank += (f[j] && c[j] < c[i]);
+    u[rank] = c[i];
+    ++nu;
+  }
+  nu = __reduce_add_sync(FULL, nu);
+  __syncwarp();
+  if (lane == 0) {  // ranges over the sorted unique columns
+    int nr = 0, off = 0, ok = 1, own0 = -1;
+    int rs = u[0], re = u[0];
+    auto close = [&](int k_end) {
+      (void)k_end;
+      if (nr < RCAP) tranges[t * RCAP + nr] = make_int2(rs, re - rs + 1);
+      off += re - rs + 1;
+      ++nr;
+    };
+    int run_off = 0;
+    for (int k = 0; k < nu; ++k) {
+      if (k > 0 && u[k] - re > WGAP + 1) {
+        close(k);
+        run_off = off;
+        rs = u[k];
+      }
+      re = u[k];
+      slot[k] = (short)(run_off + (u[k] - rs));
+      if (u[k] == r0) own0 = slot[k];
+    }
+    close(nu);
+    if (nr > RCAP || off > wrows || own0 < 0) ok = 0;
+    tinfo[t] = ok ? make_int4(nr, own0, off * rowb, 0) : make_int4(-1, 0, 0, 0);
+    s_ok[warp] = ok;
+  }
+  __syncwarp();
+  if (!s_ok[warp]) return;
+  for (int i = lane; i < E; i += 32) {
+    int rank = 0;
+    for (int j = 0; j < E; ++j) rank += (f[j] && c[j] < c[i]);
+    eslot[e0 + i] = (uint16_t)slot[rank];
+  }
+}
+
+__device__ __forceinline__ unsigned smem_addr(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}" ::"r"(smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+
+// q = A p (mode as k_spmm_pq) through TMA-staged windows.  Each half block
+// owns every other tile of the block's sweep (tiles blockIdx.x + G*(2i + h)).
+template <int KP>
+__global__ void __launch_bounds__(BLOCK, 1)
+    k_spmm_win(Ctl c, Csr A, const uint16_t* __restrict__ eslot, const int4* __restrict__ tinfo,
+               const int2* __restrict__ tranges, const double* __restrict__ P,
+               double* __restrict__ Q, int mode) {
+  using M = Map<KP>;
+  using Wn = Win<KP>;
+  constexpr int LPR = M::LPR, CPL = M::CPL, TR = Wn::TR, ROWB = Wn::ROWB, CAP = Wn::CAP;
+  extern __shared__ __align__(1024) unsigned char wsm[];  // [half][stage] windows
+  __shared__ __align__(8) uint64_t bar[2][2];
+  __shared__ double sm[M::RED];
+  __shared__ double tot[KP];
+  __shared__ int s_act[KP];
+  if (c.summary[mode == 0 ? SUM_RUN : SUM_REPLACE] == 0) return;
+  const int tid = threadIdx.x, h = tid / WHALF, ht = tid % WHALF;
+  const int gl = ht / LPR, glane = ht % LPR;
+  for (int j = tid; j < KP; j += BLOCK)
+    s_act[j] = (mode == 0) ? (c.state[j] == S_RUN) : (c.pmask[j] != 0);
+  if (ht == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[h][0])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(&bar[h][1])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  bool act[CPL];
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    act[k] = s_act[glane * CPL + k];
+    any |= act[k];
+  }
+  const int nt = (c.n + TR - 1) / TR;
+  const int my = (nt - (int)blockIdx.x + c.G - 1) / c.G;  // tiles of this block
+  const int steps = (my + 1) / 2;                          // per half (uniform)
+  auto tile_of = [&](int i) {
+    const int k = 2 * i + h;
+    return k < my ? (int)blockIdx.x + c.G * k : nt;
+  };
+  unsigned char* win0 = wsm + (size_t)h * 2 * WIN_BYTES;
+  auto issue = [&](int i) {  // producer thread: window of step i into stage i & 1
+    const int t = tile_of(i);
+    if (t >= nt) return;
+    const int4 ti = tinfo[t];
+    if (ti.x < 0) return;
+    uint64_t* b = &bar[h][i & 1];
+    unsigned char* dst = win0 + (size_t)(i & 1) * WIN_BYTES;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)),
+                 "r"(ti.z)
+                 : "memory");
+    int off = 0;
+    for (int r = 0; r < ti.x; ++r) {
+      const int2 rg = tranges[t * RCAP + r];
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_addr(dst + (size_t)off * ROWB)),
+          "l"(P + (size_t)rg.x * KP), "r"(rg.y * ROWB), "r"(smem_addr(b))
+          : "memory");
+      off += rg.y;
+    }
+  };
+  // CSR metadata pipelined one step ahead: row pointers and (slot, value) pairs
+  auto meta = [&](int i, int& row, int& st, int& ln, int& fb) {
+    const int t = tile_of(i);
+    row = -1, st = 0, ln = 0, fb = 1;
+    if (t >= nt) return;
+    fb = tinfo[t].x < 0;
+    const int rw = t * TR + gl;
+    if (rw >= c.n) return;
+    row = rw;
+    st = __ldg(A.indptr + rw);
+    ln = __ldg(A.indptr + rw + 1) - st;
+  };
+  auto entries = [&](int st, int ln, int fb, int& ci, double& cv) {
+    ci = 0;
+    cv = 0.0;
+    if (glane < ln) {
+      ci = fb ? __ldg(A.indices + st + glane) : (int)__ldg(eslot + st + glane);
+      cv = __ldg(A.val + st + glane);
+    }
+  };
+  if (ht == 0) issue(0);
+  int row, st, ln, fb, ci;
+  double cv;
+  meta(0, row, st, ln, fb);
+  entries(st, ln, fb, ci, cv);
+  int rowN, stN, lnN, fbN;
+  meta(1, rowN, stN, lnN, fbN);
+  double v[1][CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) v[0][k] = 0.0;
+  const double* Pl = P + glane * CPL;
+  unsigned phase = 0;  // bit s: parity of stage s's next completion (fallback tiles skip a use)
+  for (int i = 0; i < steps; ++i) {
+    if (ht == 0) issue(i + 1);
+    int ciN, rowNN, stNN, lnNN, fbNN;
+    double cvN;
+    entries(stN, lnN, fbN, ciN, cvN);
+    meta(i + 2, rowNN, stNN, lnNN, fbNN);
+    const int t = tile_of(i);
+    const unsigned char* win = win0 + (size_t)(i & 1) * WIN_BYTES;
+    double acc[CPL];
+#pragma unroll
+    for (int k = 0; k < CPL; ++k) acc[k] = 0.0;
+    int maxlen = (int)__reduce_max_sync(FULL, (unsigned)ln);
+    const int lim = any ? ln : 0;
+    if (!fb) {
+      if (t < nt) {
+        mbar_wait(&bar[h][i & 1], (phase >> (i & 1)) & 1u);
+        phase ^= 1u << (i & 1);
+      }
+      const double* wl = reinterpret_cast<const double*>(win) + glane * CPL;
+      for (int e = 0; e < min(maxlen, CAP); ++e) {
+        const int sl = __shfl_sync(FULL, ci, e, LPR);
+        const double vv = __shfl_sync(FULL, cv, e, LPR);
+        if (e < lim) {
+          const double* g = wl + (size_t)sl * KP;
+#pragma unroll
+          for (int k = 0; k < CPL; k += 2) {
+            const double2 gg = *reinterpret_cast<const double2*>(g + k);
+            acc[k] = fma(vv, gg.x, acc[k]);
+            acc[k + 1] = fma(vv, gg.y, acc[k + 1]);
+          }
+        }
+      }
+      for (int e = CAP; e < lim; ++e) {  // rows longer than the lane group
+        const int sl = __ldg(eslot + st + e);
+        const double vv = __ldg(A.val + st + e);
+        const double* g = wl + (size_t)sl * KP;
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) acc[k] = fma(vv, g[k], acc[k]);
+      }
+    } else {  // direct gathers
+      for (int e = 0; e < min(maxlen, CAP); ++e) {
+        const int cc = __shfl_sync(FULL, ci, e, LPR);
+        const double vv = __shfl_sync(FULL, cv, e, LPR);
+        if (e < lim) {
+          double g[CPL];
+          ldg_cols<CPL>(Pl + (size_t)cc * KP, g);
+#pragma unroll
+          for (int k = 0; k < CPL; ++k) acc[k] = fma(vv, g[k], acc[k]);
+        }
+      }
+      for (int e = CAP; e < lim; ++e) {
+        const int cc = __ldg(A.indices + st + e);
+        const double vv = __ldg(A.val + st + e);
+        double g[CPL];
+        ldg_cols<CPL>(Pl + (size_t)cc * KP, g);
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) acc[k] = fma(vv, g[k], acc[k]);
+      }
+    }
+    if (any && row >= 0) {
+      const size_t o = (size_t)row * KP + glane * CPL;
+      st_cols<CPL>(Q + o, acc);
+      double p[CPL];
+      if (!fb) {
+        const int4 ti = tinfo[t];
+        const double* g = reinterpret_cast<const double*>(win) +
+                          (size_t)(ti.y + row - t * TR) * KP + glane * CPL;
+#pragma unroll
+        for (int k = 0; k < CPL; ++k) p[k] = g[k];
+      } else {
+        ldg_cols<CPL>(P + o, p);
+      }
+#pragma unroll
+      for (int k = 0; k < CPL; ++k)
+        if (act[k]) v[0][k] += p[k] * acc[k];
+    }
+    asm volatile("bar.sync %0, %1;" ::"r"(1 + h), "r"(WHALF) : "memory");  // stage i&1 free
+    row = rowN;
+    st = stN;
+    ln = lnN;
+    fb = fbN;
+    ci = ciN;
+    cv = cvN;
+    rowN = rowNN;
+    stN = stNN;
+    lnN = lnNN;
+    fbN = fbNN;
+  }
+  block_partials<KP, 1>(v, sm, c.part0, nullptr);
+  if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
+  if (tid < KP) {
+    if (s_act[tid]) c.alpha[tid] = c.rz[tid] / tot[tid];
+  }
+}
+
 // ---------------------------------------------------------------- fused x/p update + SpMM
 // One launch does round k's  x += alpha p, p = r/d + beta p  and round k+1's
 // q = A p, p.q.  Rows are grouped in bands of G*tpb tiles.  Every block first
@@ -1042,10 +1351,18 @@ struct Layout {
   int* summary;
   int* xdone;  // k_xs band counters (one per band; bands <= tiles)
   int* bw;     // matrix bandwidth scratch
+  int4* tinfo;       // k_spmm_win tile windows
+  int2* tranges;
+  uint16_t* eslot;
   size_t bytes;
 };
 
-inline Layout carve(void* ws, int n, int kp) {
+inline int win_tile_rows(int kp) {  // Win<KP>::TR
+  const int lpr = (kp >= 4) ? kp / 4 : kp / 2;
+  return WHALF / lpr;
+}
+
+inline Layout carve(void* ws, int n, int kp, int64_t nnz) {
   Carve cv{reinterpret_cast<char*>(ws), 0, ~size_t(0)};
   Layout L;
   const size_t nk = (size_t)n * kp;
@@ -1072,6 +1389,10 @@ inline Layout carve(void* ws, int n, int kp) {
   L.summary = cv.take<int>(SUM_N);
   L.xdone = cv.take<int>((size_t)n + 2);
   L.bw = cv.take<int>(2);
+  const size_t ntw = (size_t)(n + win_tile_rows(kp) - 1) / win_tile_rows(kp);
+  L.tinfo = cv.take<int4>(ntw + 1);
+  L.tranges = cv.take<int2>((ntw + 1) * RCAP);
+  L.eslot = cv.take<uint16_t>((size_t)nnz + 8);
   L.bytes = cv.used + 256;
   return L;
 }
@@ -1095,9 +1416,18 @@ inline bool fused_enabled() {
 
 // Control block and grids for one solve.  c: streaming kernels; cs: SpMM and
 // fused kernels (one block per SM for 4-column lanes) with the band schedule.
+// The TMA-windowed SpMM (k_spmm_win) is correct but, with one window in
+// flight per half block, it waits on its mbarriers ~35% of the time and runs
+// at 0.54 ms vs 0.33 ms for the register-pipelined gathers (C2, kp=64).
+// Opt in with HFB200_WIN=1 while its pipeline is deepened.
+inline bool win_enabled() {
+  const char* v = getenv("HFB200_WIN");
+  return v && v[0] == '1';
+}
+
 template <int KP>
 int setup(const Layout& L, const hf_csr* A, int n, double tol, int max_iter, Ctl& c, Ctl& cs,
-          bool& fused, cudaStream_t stream) {
+          bool& fused, bool& win, cudaStream_t stream) {
   memset(&c, 0, sizeof(c));
   c.n = n;
   c.kp = KP;
@@ -1111,7 +1441,20 @@ int setup(const Layout& L, const hf_csr* A, int n, double tol, int max_iter, Ctl
   c.counter = L.counter; c.summary = L.summary; c.xdone = L.xdone;
   cs = c;
   cs.G = grid_for(n, KP, Spmm<KP>::BPS);
-  fused = Spmm<KP>::PIPELINED && fused_enabled();
+  win = (KP >= 32) && win_enabled();
+  if (win) {  // per-tile TMA windows of the SpMM (once per solve)
+    const int tr = Win<KP>::TR;
+    const int ntw = (n + tr - 1) / tr;
+    k_plan_windows<<<(ntw + 7) / 8, 256, 0, stream>>>(n, tr, Win<KP>::WROWS, Win<KP>::ROWB,
+                                                       A->indptr, A->indices, L.tinfo, L.tranges,
+                                                       L.eslot);
+    HF_LAUNCH_CHECK();
+    count_launches(1);
+    HF_CUDA(cudaFuncSetAttribute(k_spmm_win<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 4 * WIN_BYTES));
+    cs.G = grid_for(n, KP, 1);
+  }
+  fused = Spmm<KP>::PIPELINED && fused_enabled() && !win;
   if (fused) {  // band schedule from the matrix bandwidth (max |col - row|)
     HF_CUDA(cudaMemsetAsync(L.bw, 0, sizeof(int), stream));
     k_bandwidth<<<(n + 255) / 256, 256, 0, stream>>>(n, A->indptr, A->indices, L.bw);
@@ -1150,15 +1493,15 @@ template <int KP>
 int run(const hf_csr* A, const double* d, const double* B, int n, double tol, int max_iter,
         const int32_t* freeze_at, double* X, int32_t* iters, int32_t* status, double* true_res,
         double* best_res, int32_t* best_iter, void* ws, size_t ws_bytes, cudaStream_t stream) {
-  Layout L = carve(ws, n, KP);
+  Layout L = carve(ws, n, KP, A->nnz);
   if (L.bytes > ws_bytes) {
     set_error("pcg workspace too small: need %zu, have %zu", L.bytes, ws_bytes);
     return HF_ERR_WORKSPACE;
   }
   Ctl c, cs;
-  bool fused = false;
+  bool fused = false, win = false;
   Csr csr{A->indptr, A->indices, A->val};
-  if (int rc = setup<KP>(L, A, n, tol, max_iter, c, cs, fused, stream)) return rc;
+  if (int rc = setup<KP>(L, A, n, tol, max_iter, c, cs, fused, win, stream)) return rc;
   if (freeze_at != nullptr) {
     HF_CUDA(cudaMemcpyAsync(L.freeze, freeze_at, sizeof(int) * KP, cudaMemcpyDeviceToDevice, stream));
     c.freeze = L.freeze;
@@ -1207,7 +1550,11 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
         cudaError_t e = launch_xs<KP>(cs, csr, X, L.P, L.R, L.Q, guard.cs);
         if (e != cudaSuccess) le = e;
       } else {
-        k_spmm_pq<KP><<<cs.G, BLOCK, 0, guard.cs>>>(cs, csr, L.P, L.Q, 0);
+        if (win)
+          k_spmm_win<KP><<<cs.G, BLOCK, 4 * WIN_BYTES, guard.cs>>>(cs, csr, L.eslot, L.tinfo,
+                                                                   L.tranges, L.P, L.Q, 0);
+        else
+          k_spmm_pq<KP><<<cs.G, BLOCK, 0, guard.cs>>>(cs, csr, L.P, L.Q, 0);
         k_update_r<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, L.Q, L.R);
         k_update_xp<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, SUM_MASKED, X, L.P, L.R);
       }
@@ -1269,15 +1616,15 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
 template <int KP>
 int profile(const hf_csr* A, const double* d, const double* B, int n, int rounds, double* X,
             float* ms3, int* fused_out, void* ws, size_t ws_bytes, cudaStream_t stream) {
-  Layout L = carve(ws, n, KP);
+  Layout L = carve(ws, n, KP, A->nnz);
   if (L.bytes > ws_bytes) {
     set_error("pcg workspace too small");
     return HF_ERR_WORKSPACE;
   }
   Ctl c, cs;
-  bool fused = false;
+  bool fused = false, win = false;
   Csr csr{A->indptr, A->indices, A->val};
-  if (int rc = setup<KP>(L, A, n, 0.0, 1 << 30, c, cs, fused, stream)) return rc;
+  if (int rc = setup<KP>(L, A, n, 0.0, 1 << 30, c, cs, fused, win, stream)) return rc;
   *fused_out = fused ? 1 : 0;
   HF_CUDA(cudaMemsetAsync(L.counter, 0, sizeof(unsigned int) * 4, stream));
   k_init<KP><<<c.G, BLOCK, 0, stream>>>(c, B, d, X, L.R, L.P);
@@ -1297,7 +1644,11 @@ int profile(const hf_csr* A, const double* d, const double* B, int n, int rounds
       cudaEventRecord(ev[3], stream);
     } else {
       cudaEventRecord(ev[0], stream);
-      k_spmm_pq<KP><<<cs.G, BLOCK, 0, stream>>>(cs, csr, L.P, L.Q, 0);
+      if (win)
+        k_spmm_win<KP><<<cs.G, BLOCK, 4 * WIN_BYTES, stream>>>(cs, csr, L.eslot, L.tinfo,
+                                                               L.tranges, L.P, L.Q, 0);
+      else
+        k_spmm_pq<KP><<<cs.G, BLOCK, 0, stream>>>(cs, csr, L.P, L.Q, 0);
       cudaEventRecord(ev[1], stream);
       k_update_r<KP><<<c.G, BLOCK, 0, stream>>>(c, L.Q, L.R);
       cudaEventRecord(ev[2], stream);
@@ -1364,8 +1715,8 @@ __global__ void k_prune_fill(int n, const int32_t* __restrict__ indptr,
 
 using namespace hf;
 
-extern "C" size_t hf_pcg_workspace_bytes(int32_t n, int32_t kp) {
-  return pcg::carve(nullptr, n, kp).bytes;
+extern "C" size_t hf_pcg_workspace_bytes(int32_t n, int32_t kp, int64_t nnz) {
+  return pcg::carve(nullptr, n, kp, nnz).bytes;
 }
 
 extern "C" int hf_pcg_multi(const hf_csr* A, const double* d, const double* B, int32_t n,

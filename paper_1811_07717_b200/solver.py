@@ -86,7 +86,7 @@ def _run_batch(op, Bb, tol, max_iter, freeze=None):
     """One hf_pcg_multi call on an n x kp block; returns X and host arrays."""
     n, kp = Bb.shape
     X = torch.empty_like(Bb)
-    ws = torch.empty(N.lib.hf_pcg_workspace_bytes(n, kp), dtype=torch.uint8, device=Bb.device)
+    ws = torch.empty(N.lib.hf_pcg_workspace_bytes(n, kp, op.Ac.nnz), dtype=torch.uint8, device=Bb.device)
     it = np.zeros(kp, dtype=np.int32)
     stt = np.zeros(kp, dtype=np.int32)
     tr = np.zeros(kp, dtype=np.float64)

@@ -201,6 +201,23 @@ class TestTransferMatrix:
         T1 = eng.transfer_matrix(A, B)
         np.testing.assert_array_equal(T0, T1)
 
+    def test_tma_window_spmm_matches(self, eng, monkeypatch):
+        """The TMA-windowed SpMM (HFB200_WIN=1) sums the same entries in the
+        same order: transfer columns agree to the reduction-order rounding."""
+        from tests.fixtures import csr
+
+        fx = load("c1.npz")
+        from tests.fixtures import electrodes_from_fixture, mesh_from_fixture
+
+        mesh = mesh_from_fixture(fx)
+        A = eng.assemble_A(mesh, electrodes_from_fixture(mesh, fx))
+        B = csr(fx, "B").toarray()
+        monkeypatch.setenv("HFB200_WIN", "0")
+        T0 = eng.transfer_matrix(A, B)
+        monkeypatch.setenv("HFB200_WIN", "1")
+        T1 = eng.transfer_matrix(A, B)
+        assert np.linalg.norm(T1 - T0) / np.linalg.norm(T0) < 1e-12
+
     def test_iterations_match_reference_per_column(self, eng):
         from paper_1811_07717_b200.solver import operator, rhs_block, solve_block
         from tests.fixtures import csr

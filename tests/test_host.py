@@ -47,7 +47,7 @@ def test_library_is_sm100a():
 def test_workspace_queries_need_no_gpu():
     from paper_1811_07717_b200 import _native as N
 
-    assert N.lib.hf_pcg_workspace_bytes(1000, 32) > 1000 * 32 * 8 * 3
+    assert N.lib.hf_pcg_workspace_bytes(1000, 32, 15000) > 1000 * 32 * 8 * 3
     assert N.lib.hf_p1_assemble_workspace_bytes(1000, 5000, 10) > 0
     assert N.lib.hf_csr_prune_workspace_bytes(1000) > 0
 
