@@ -944,26 +944,44 @@ __global__ void __launch_bounds__(BLOCK, 1)
     return k < my ? (int)blockIdx.x + c.G * k : nt;
   };
   unsigned char* win0 = wsm + (size_t)h * 2 * WIN_BYTES;
-  auto issue = [&](int i) {  // producer thread: window of step i into stage i & 1
+  // Producer = warp 0 of the half.  The window descriptor of step i+1 (tile
+  // info in every lane, range r in lane r) is loaded one step early, so the
+  // copies for step i+1 issue at the top of step i without a dependent load.
+  const bool pw = ht < 32;
+  const int lane = ht & 31;
+  int4 ninfo = make_int4(-1, 0, 0, 0);
+  int2 nrng = make_int2(0, 0);
+  auto load_desc = [&](int i) {
     const int t = tile_of(i);
-    if (t >= nt) return;
-    const int4 ti = tinfo[t];
-    if (ti.x < 0) return;
+    ninfo = make_int4(-1, 0, 0, 0);
+    nrng = make_int2(0, 0);
+    if (t < nt) {
+      ninfo = tinfo[t];
+      if (lane < RCAP && ninfo.x > lane) nrng = tranges[t * RCAP + lane];
+    }
+  };
+  auto issue = [&](int i) {  // warp 0: window of step i (descriptor in ninfo/nrng) into stage i & 1
+    if (ninfo.x < 0) return;
     uint64_t* b = &bar[h][i & 1];
     unsigned char* dst = win0 + (size_t)(i & 1) * WIN_BYTES;
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)),
-                 "r"(ti.z)
-                 : "memory");
     int off = 0;
-    for (int r = 0; r < ti.x; ++r) {
-      const int2 rg = tranges[t * RCAP + r];
-      asm volatile(
-          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-              smem_addr(dst + (size_t)off * ROWB)),
-          "l"(P + (size_t)rg.x * KP), "r"(rg.y * ROWB), "r"(smem_addr(b))
-          : "memory");
-      off += rg.y;
+    for (int r = 0; r < ninfo.x; ++r) {
+      const int st = __shfl_sync(FULL, nrng.x, r);
+      const int len = __shfl_sync(FULL, nrng.y, r);
+      if (lane == 0) {
+        if (r == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)),
+                       "r"(ninfo.z)
+                       : "memory");
+        }
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                smem_addr(dst + (size_t)off * ROWB)),
+            "l"(P + (size_t)st * KP), "r"(len * ROWB), "r"(smem_addr(b))
+            : "memory");
+      }
+      off += len;
     }
   };
   // CSR metadata pipelined one step ahead: row pointers and (slot, value) pairs
@@ -986,7 +1004,11 @@ __global__ void __launch_bounds__(BLOCK, 1)
       cv = __ldg(A.val + st + glane);
     }
   };
-  if (ht == 0) issue(0);
+  if (pw) {
+    load_desc(0);
+    issue(0);
+    load_desc(1);
+  }
   int row, st, ln, fb, ci;
   double cv;
   meta(0, row, st, ln, fb);
@@ -999,7 +1021,10 @@ __global__ void __launch_bounds__(BLOCK, 1)
   const double* Pl = P + glane * CPL;
   unsigned phase = 0;  // bit s: parity of stage s's next completion (fallback tiles skip a use)
   for (int i = 0; i < steps; ++i) {
-    if (ht == 0) issue(i + 1);
+    if (pw) {
+      issue(i + 1);
+      load_desc(i + 2);
+    }
     int ciN, rowNN, stNN, lnNN, fbNN;
     double cvN;
     entries(stN, lnN, fbN, ciN, cvN);
