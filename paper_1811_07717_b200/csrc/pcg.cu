@@ -40,7 +40,8 @@ namespace pcg {
 constexpr int BLOCK = 512;
 constexpr int NWARP = BLOCK / 32;
 constexpr int BLOCKS_PER_SM = 2;
-constexpr int CHUNK = 8;  // PCG rounds per captured graph
+constexpr int CHUNK = 8;      // PCG rounds per captured graph
+constexpr int LOOKAHEAD = 3;  // chunks queued beyond the one whose status is read
 
 enum : int {
   S_RUN = 0,
@@ -1549,7 +1550,7 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
     cudaGraph_t g = nullptr;
     cudaGraphExec_t ge = nullptr;
     cudaStream_t cs = nullptr;
-    cudaEvent_t ev[2] = {nullptr, nullptr};
+    cudaEvent_t ev[LOOKAHEAD + 1] = {};
     ~Guard() {
       if (ge) cudaGraphExecDestroy(ge);
       if (g) cudaGraphDestroy(g);
@@ -1595,20 +1596,22 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
       return HF_ERR_CUDA;
     }
     HF_CUDA(cudaGraphInstantiate(&guard.ge, guard.g, 0));
-    HF_CUDA(cudaEventCreateWithFlags(&guard.ev[0], cudaEventDisableTiming));
-    HF_CUDA(cudaEventCreateWithFlags(&guard.ev[1], cudaEventDisableTiming));
+    for (auto& e : guard.ev) HF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     const long per_chunk = fused ? 2 * CHUNK + 4 : 3 * CHUNK + 3;
     // Every chunk costs at least one iteration of some column (or finishes a
     // CHECK); bound the loop generously and report if control never settles.
     const long max_chunks = 4L * (max_iter / CHUNK + 2) + 64;
     long i = 0;
     bool finished = false;
+    // Keep LOOKAHEAD chunks queued ahead of the status being read, so a late
+    // host wake-up never leaves the GPU idle; chunks queued after the last
+    // column finished exit at once (every kernel is gated on the status).
     for (; i < max_chunks; ++i) {
       HF_CUDA(cudaGraphLaunch(guard.ge, stream));
       count_launches(per_chunk);
-      HF_CUDA(cudaEventRecord(guard.ev[i & 1], stream));
-      if (i >= 1) {
-        HF_CUDA(cudaEventSynchronize(guard.ev[(i - 1) & 1]));
+      HF_CUDA(cudaEventRecord(guard.ev[i % (LOOKAHEAD + 1)], stream));
+      if (i >= LOOKAHEAD) {
+        HF_CUDA(cudaEventSynchronize(guard.ev[(i - LOOKAHEAD) % (LOOKAHEAD + 1)]));
         volatile int* hs = h_sum;
         if (hs[SUM_RUN] == 0 && hs[SUM_CHECK] == 0) {
           finished = true;
