@@ -29,6 +29,7 @@
 #include <math.h>
 
 #include <algorithm>
+#include <vector>
 #include <stdlib.h>
 #include <string.h>
 
@@ -1543,8 +1544,13 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
     count_launches(1);
   }
 
-  int* h_sum = nullptr;
-  HF_CUDA(cudaHostAlloc(&h_sum, sizeof(int) * SUM_N, cudaHostAllocDefault));
+  // Pinned status words and the capture stream are allocated once per host
+  // thread and reused: cudaHostAlloc can stall for tens of milliseconds.
+  static thread_local int* h_sum_tls = nullptr;
+  static thread_local cudaStream_t cap_tls = nullptr;
+  if (!h_sum_tls) HF_CUDA(cudaHostAlloc(&h_sum_tls, sizeof(int) * SUM_N, cudaHostAllocDefault));
+  if (!cap_tls) HF_CUDA(cudaStreamCreateWithFlags(&cap_tls, cudaStreamNonBlocking));
+  int* h_sum = h_sum_tls;
   struct Guard {
     int* h;
     cudaGraph_t g = nullptr;
@@ -1554,10 +1560,8 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
     ~Guard() {
       if (ge) cudaGraphExecDestroy(ge);
       if (g) cudaGraphDestroy(g);
-      if (cs) cudaStreamDestroy(cs);
       for (auto e : ev)
         if (e) cudaEventDestroy(e);
-      if (h) cudaFreeHost(h);
     }
   } guard{h_sum};
   HF_CUDA(cudaMemcpyAsync(h_sum, L.summary, sizeof(int) * SUM_N, cudaMemcpyDeviceToHost, stream));
@@ -1567,36 +1571,48 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
     // Capture one chunk: CHUNK rounds, then the check path, then the status copy.
     // Unfused round: spmm_pq, update_r, update_xp.  Fused round: update_r,
     // k_xs (= update_xp of this round + spmm_pq of the next).
-    HF_CUDA(cudaStreamCreateWithFlags(&guard.cs, cudaStreamNonBlocking));
-    HF_CUDA(cudaStreamBeginCapture(guard.cs, cudaStreamCaptureModeThreadLocal));
-    cudaError_t le = cudaSuccess;
-    for (int r = 0; r < CHUNK; ++r) {
-      if (fused) {
-        k_update_r<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, L.Q, L.R);
-        cudaError_t e = launch_xs<KP>(cs, csr, X, L.P, L.R, L.Q, guard.cs);
-        if (e != cudaSuccess) le = e;
-      } else {
-        if (win)
-          k_spmm_win<KP><<<cs.G, BLOCK, 4 * WIN_BYTES, guard.cs>>>(cs, csr, L.eslot, L.tinfo,
-                                                                   L.tranges, L.P, L.Q, 0);
-        else
-          k_spmm_pq<KP><<<cs.G, BLOCK, 0, guard.cs>>>(cs, csr, L.P, L.Q, 0);
-        k_update_r<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, L.Q, L.R);
-        k_update_xp<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, SUM_MASKED, X, L.P, L.R);
+    auto enqueue_chunk = [&](cudaStream_t q) -> cudaError_t {
+      cudaError_t le = cudaSuccess;
+      for (int r = 0; r < CHUNK; ++r) {
+        if (fused) {
+          k_update_r<KP><<<c.G, BLOCK, 0, q>>>(c, L.Q, L.R);
+          cudaError_t e = launch_xs<KP>(cs, csr, X, L.P, L.R, L.Q, q);
+          if (e != cudaSuccess) le = e;
+        } else {
+          if (win)
+            k_spmm_win<KP><<<cs.G, BLOCK, 4 * WIN_BYTES, q>>>(cs, csr, L.eslot, L.tinfo, L.tranges,
+                                                               L.P, L.Q, 0);
+          else
+            k_spmm_pq<KP><<<cs.G, BLOCK, 0, q>>>(cs, csr, L.P, L.Q, 0);
+          k_update_r<KP><<<c.G, BLOCK, 0, q>>>(c, L.Q, L.R);
+          k_update_xp<KP><<<c.G, BLOCK, 0, q>>>(c, SUM_MASKED, X, L.P, L.R);
+        }
       }
+      k_spmm_resid<KP><<<cs.G, BLOCK, 0, q>>>(cs, csr, B, X, L.Q);
+      k_replace<KP><<<c.G, BLOCK, 0, q>>>(c, L.Q, L.R);
+      k_update_xp<KP><<<c.G, BLOCK, 0, q>>>(c, SUM_REPLACE, X, L.P, L.R);
+      if (fused) k_spmm_pq<KP><<<cs.G, BLOCK, 0, q>>>(cs, csr, L.P, L.Q, 1);
+      cudaMemcpyAsync(h_sum, L.summary, sizeof(int) * SUM_N, cudaMemcpyDeviceToHost, q);
+      return le;
+    };
+    const char* ng = getenv("HFB200_NOGRAPH");
+    const bool use_graph = !(ng && ng[0] == '1');
+    if (use_graph) {
+      guard.cs = cap_tls;
+      HF_CUDA(cudaStreamBeginCapture(guard.cs, cudaStreamCaptureModeThreadLocal));
+      cudaError_t le = enqueue_chunk(guard.cs);
+      cudaError_t ce = cudaStreamEndCapture(guard.cs, &guard.g);
+      if (ce != cudaSuccess || le != cudaSuccess) {
+        set_error("graph capture failed: %s / %s", cudaGetErrorString(ce), cudaGetErrorString(le));
+        return HF_ERR_CUDA;
+      }
+      HF_CUDA(cudaGraphInstantiate(&guard.ge, guard.g, 0));
     }
-    k_spmm_resid<KP><<<cs.G, BLOCK, 0, guard.cs>>>(cs, csr, B, X, L.Q);
-    k_replace<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, L.Q, L.R);
-    k_update_xp<KP><<<c.G, BLOCK, 0, guard.cs>>>(c, SUM_REPLACE, X, L.P, L.R);
-    if (fused) k_spmm_pq<KP><<<cs.G, BLOCK, 0, guard.cs>>>(cs, csr, L.P, L.Q, 1);
-    cudaMemcpyAsync(h_sum, L.summary, sizeof(int) * SUM_N, cudaMemcpyDeviceToHost, guard.cs);
-    cudaError_t ce = cudaStreamEndCapture(guard.cs, &guard.g);
-    if (ce != cudaSuccess || le != cudaSuccess) {
-      set_error("graph capture failed: %s / %s", cudaGetErrorString(ce), cudaGetErrorString(le));
-      return HF_ERR_CUDA;
-    }
-    HF_CUDA(cudaGraphInstantiate(&guard.ge, guard.g, 0));
     for (auto& e : guard.ev) HF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    // HFB200_TRACE=1: per-chunk GPU durations on stderr (diagnostics only)
+    const char* tr = getenv("HFB200_TRACE");
+    const bool trace = tr && tr[0] == '1';
+    std::vector<cudaEvent_t> tev;
     const long per_chunk = fused ? 2 * CHUNK + 4 : 3 * CHUNK + 3;
     // Every chunk costs at least one iteration of some column (or finishes a
     // CHECK); bound the loop generously and report if control never settles.
@@ -1607,7 +1623,17 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
     // host wake-up never leaves the GPU idle; chunks queued after the last
     // column finished exit at once (every kernel is gated on the status).
     for (; i < max_chunks; ++i) {
-      HF_CUDA(cudaGraphLaunch(guard.ge, stream));
+      if (trace) {
+        tev.emplace_back();
+        cudaEventCreate(&tev.back());
+        cudaEventRecord(tev.back(), stream);
+      }
+      if (use_graph) {
+        HF_CUDA(cudaGraphLaunch(guard.ge, stream));
+      } else {
+        HF_CUDA(enqueue_chunk(stream));
+        HF_LAUNCH_CHECK();
+      }
       count_launches(per_chunk);
       HF_CUDA(cudaEventRecord(guard.ev[i % (LOOKAHEAD + 1)], stream));
       if (i >= LOOKAHEAD) {
@@ -1620,6 +1646,16 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
       }
     }
     HF_CUDA(cudaStreamSynchronize(stream));
+    if (trace && tev.size() > 1) {
+      fprintf(stderr, "[hfb200] chunk ms:");
+      for (size_t k = 1; k < tev.size(); ++k) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, tev[k - 1], tev[k]);
+        fprintf(stderr, " %.2f", ms);
+      }
+      fprintf(stderr, "\n");
+      for (auto e : tev) cudaEventDestroy(e);
+    }
     if (!finished) {
       volatile int* hs = h_sum;
       if (!(hs[SUM_RUN] == 0 && hs[SUM_CHECK] == 0)) {
