@@ -25,6 +25,8 @@
  *   hf_lf_tail             leadfield.py:122-134 eeg_leadfield: L = W (G'T)'  with W = -R M^-1
  *   hf_dense_lf            leadfield.py:230-237 eit_leadfield column blocks  W Q[p]'
  *   hf_eit_sens            leadfield.py:179-207 _dof_sensitivities: Q[p,m,:] = T' K_m u_p
+ *   hf_boundary_faces      meshgen.py:101-134  TetMesh.boundary_triangles
+ *   hf_whitney_gt          fem.py:291-422      assemble_G (Whitney source matrix), as G'
  *
  * See INTEGRATION.md for the ctypes binding the reference would use.
  */
@@ -189,6 +191,29 @@ int hf_eit_sens(const double* nodes, const int32_t* tetra, const int32_t* dof_el
                 const int32_t* dof_ptr, int32_t n_dofs, int32_t ground, const double* T,
                 int32_t ldt, int32_t L, const double* U, int32_t ldu, int32_t P, double* Q,
                 void* stream);
+
+/* ---------------------------------------------------------------- topology (next rows, §8f) */
+
+/* Boundary faces of a tetrahedral mesh (meshgen.py:101-134): face k of element e
+ * is opposite local vertex k, ids f = 4e + k; a face is on the boundary when no
+ * other element holds its three nodes.  face_idx (device, capacity 4m) receives
+ * the boundary face ids ascending (the reference's flatnonzero order);
+ * *n_faces (host) their number.  ws: hf_topology_workspace_bytes(n, m, 0). */
+size_t hf_topology_workspace_bytes(int32_t n, int32_t m, int32_t ncols);
+int hf_boundary_faces(const int32_t* tetra, int32_t n, int32_t m, int32_t* face_idx,
+                      int64_t* n_faces, void* ws, size_t ws_bytes, void* stream);
+
+/* Source matrix G of assemble_G (fem.py:291-422) as its transpose G' in CSR:
+ * row c = source column c (3 per source, x/y/z, unconstrained; or 1 per source
+ * when orient (device S x 3) is given, constrained), columns = mesh nodes
+ * ascending (the <= 8 nodes of the source element and its face neighbours).
+ * Two calls: with gidx/gval NULL it writes gptr (device, ncols+1) and *nnz_out;
+ * then with gidx/gval (device, nnz) it fills them.
+ * ws: hf_topology_workspace_bytes(n, m, ncols). */
+int hf_whitney_gt(const double* nodes, const int32_t* tetra, int32_t n, int32_t m,
+                  const int32_t* src_elems, int32_t n_src, const double* orient, int32_t* gptr,
+                  int32_t* gidx, double* gval, int64_t* nnz_out, void* ws, size_t ws_bytes,
+                  void* stream);
 
 #ifdef __cplusplus
 }

@@ -322,7 +322,7 @@ inline Ws carve(void* base, int n, int m, int nt) {
   return w;
 }
 
-inline int build_incidence(const int32_t* conn, int width, int count, int n, int32_t* cnt,
+int build_incidence(const int32_t* conn, int width, int count, int n, int32_t* cnt,
                            int32_t* off, int32_t* cur, int32_t* inc, int32_t* scratch,
                            int32_t* tot, cudaStream_t s) {
   HF_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t) * (n + 1), s));

@@ -45,13 +45,15 @@ class EegEngine:
 
     def __init__(self, mesh, electrodes, G, cfg=PcgConfig(), B=None, C=None, R=None,
                  columns=None, dev=None):
+        """G: n x ncols (scipy / ndarray), G' already in HBM (DeviceCsr, ncols x n), or a
+        SourceSpace, in which case G' is assembled on the device (fem.py:391-422)."""
         dev = dev or device()
         self.cfg = cfg
         self.h2d_bytes = 0
         self.dmesh = DeviceMesh(mesh.nodes, mesh.tetra, dev)
         self.h2d_bytes += self.dmesh.nodes.numel() * 8 + self.dmesh.tetra.numel() * 4
-        sig = np.asarray(mesh.sigma, dtype=np.float64)
-        self.sigma = torch.from_numpy(np.ascontiguousarray(sig)).to(dev)
+        sig = np.array(mesh.sigma, dtype=np.float64, order="C")
+        self.sigma = torch.from_numpy(sig).to(dev)
         self.h2d_bytes += sig.nbytes
         if B is None or C is None or R is None:
             B, C, R = model.assemble_B_C_R(mesh, electrodes)
@@ -68,9 +70,19 @@ class EegEngine:
         self.Bt = DeviceCsr.from_scipy(sp.csr_matrix(sp.csr_matrix(B).T), dev)
         self.Cdiag = torch.from_numpy(np.ascontiguousarray(C.diagonal(), dtype=np.float64)).to(dev)
         self.R = np.asarray(R, dtype=np.float64)
-        Gs = G if sp.issparse(G) else sp.csr_matrix(np.asarray(G, dtype=float))
-        self.Gt = DeviceCsr.from_scipy(sp.csr_matrix(Gs.T), dev)
-        self.ncols = Gs.shape[1]
+        if isinstance(G, DeviceCsr):  # already G' in HBM (topology.assemble_Gt_device)
+            self.Gt = G
+            self.ncols = G.shape[0]
+        elif hasattr(G, "element_ids"):  # a SourceSpace: assemble G' on the device
+            from .topology import assemble_Gt_device
+
+            self.Gt = assemble_Gt_device(mesh, G)
+            self.ncols = self.Gt.shape[0]
+            self.h2d_bytes += 4 * len(G.element_ids)
+        else:
+            Gs = G if sp.issparse(G) else sp.csr_matrix(np.asarray(G, dtype=float))
+            self.Gt = DeviceCsr.from_scipy(sp.csr_matrix(Gs.T), dev)
+            self.ncols = Gs.shape[1]
         self.h2d_bytes += (Bc.nnz * 20 + self.Bt.nnz * 12 + self.Gt.nnz * 12 + 8 * self.L
                            + 4 * (self.n + 1) + 4 * (self.ncols + 1) + 4 * (self.L + 1))
         self.last_info = None
@@ -109,6 +121,7 @@ class EegEngine:
         return LF.cpu().numpy() if to_host else LF
 
 
-def eeg_leadfield_from_mesh(mesh, electrodes, G, cfg=PcgConfig()):
-    """Host mesh/electrodes/G in, host lead field (L x ncols) out — the e2e call."""
-    return EegEngine(mesh, electrodes, G, cfg).build(to_host=True)
+def eeg_leadfield_from_mesh(mesh, electrodes, sources, cfg=PcgConfig()):
+    """Host mesh, electrodes and sources (a SourceSpace, or G itself) in, host
+    lead field (L x ncols) out: assemble_cem_system + eeg_leadfield in one call."""
+    return EegEngine(mesh, electrodes, sources, cfg).build(to_host=True)

@@ -64,7 +64,7 @@ def blocks_device(dmesh, sigma_arr, sigma_scalar, elements=None):
     if torch.is_tensor(sigma_arr):  # already resident (engine.EegEngine)
         sg, cols = sigma_arr, (1 if sigma_arr.dim() == 1 else 6)
     elif sigma_arr is not None:
-        sg = torch.from_numpy(np.ascontiguousarray(sigma_arr, dtype=np.float64)).to(dev)
+        sg = torch.from_numpy(np.array(sigma_arr, dtype=np.float64, order="C")).to(dev)
         cols = 1 if sigma_arr.ndim == 1 else 6
     blocks = torch.empty(m_sub * 16 + 1, dtype=torch.float64, device=dev)
     flags = N.C.c_int32(0)

@@ -86,8 +86,12 @@ class EegProblem:
     name: str
 
 
-def eeg_problem(name="c2", n_electrodes=None, n_sources=None, h=None, seed=1):
-    """C1 / C2 EEG problem: mesh, electrodes, unconstrained sources, G, B, C, R."""
+def eeg_problem(name="c2", n_electrodes=None, n_sources=None, h=None, seed=1, device=False,
+                with_G=True):
+    """C1 / C2 / C5 EEG problem: mesh, electrodes, unconstrained sources, G, B, C, R.
+
+    device=True builds the boundary faces and the source matrix with the CUDA
+    kernels (G is then G' in HBM, a DeviceCsr); otherwise on the host."""
     if name == "c1":
         radii, cond = C1_RADII, C1_COND
         h = h or 0.004
@@ -103,10 +107,16 @@ def eeg_problem(name="c2", n_electrodes=None, n_sources=None, h=None, seed=1):
     else:
         raise ValueError(name)
     mesh = sphere_mesh(radii, cond, h)
+    if device:  # boundary faces and G' from the device kernels (topology.py)
+        from .topology import assemble_Gt_device, boundary_triangles_device
+
+        mesh._boundary = boundary_triangles_device(mesh)
     el = model.ElectrodeSet.from_centers(mesh, fibonacci_sphere_points(L, radii[-1]), radius=rad,
                                          impedances=1e3)
     src = model.place_sources(mesh, [0], S, seed=seed)
-    G = model.assemble_G(mesh, src)
+    G = None
+    if with_G:
+        G = assemble_Gt_device(mesh, src) if device else model.assemble_G(mesh, src)
     B, C, R = model.assemble_B_C_R(mesh, el)
     g = model.ground_node(mesh, el)
     return EegProblem(mesh, el, src, G, B, C, R, g, name)

@@ -18,7 +18,7 @@ ap.add_argument("--config", default="c2")
 ap.add_argument("--rounds", type=int, default=3)
 ap.add_argument("--build", action="store_true")
 args = ap.parse_args()
-prob = synthetic.eeg_problem(args.config)
+prob = synthetic.eeg_problem(args.config, device=True)
 eng = EegEngine(prob.mesh, prob.electrodes, prob.G, PcgConfig(1e-8), prob.B, prob.C, prob.R)
 A = eng.assemble()
 if args.build:
