@@ -79,7 +79,7 @@ struct Csr {
 
 template <int KP>
 struct Map {
-  static constexpr int CPL = (KP >= 4) ? 4 : 2;  // columns per lane: one 256-bit access
+  static constexpr int CPL = (KP >= 64) ? 4 : 2;  // columns per lane: one 256/128-bit access
   static constexpr int LPR = KP / CPL;            // lanes per row
   static constexpr int RB = BLOCK / LPR;                    // rows per block pass
   static constexpr int SPLIT = BLOCK / KP;                  // last-block reduction splits
@@ -298,10 +298,10 @@ struct Spmm {
   static constexpr int R = 1;  // rows per row group per step (pipelined across steps)
   // 4-column lanes hold 8 x 256-bit gathers in registers: one block per SM
   // with a 128-register budget; 2-column lanes fit two blocks per SM.
-  static constexpr int BPS = (Map<KP>::CPL == 4) ? 1 : 2;
+  static constexpr int BPS = (Map<KP>::LPR >= 4) ? 1 : 2;
   // (index, value) pairs each lane of a row group holds for the pipeline
-  static constexpr int EPL = (Map<KP>::LPR >= 16) ? 1 : 2;
-  static constexpr bool PIPELINED = Map<KP>::LPR >= 8;
+  static constexpr int EPL = (Map<KP>::LPR >= 16) ? 1 : 2;  // CAP = LPR*EPL >= 8 entries
+  static constexpr bool PIPELINED = Map<KP>::LPR >= 4;
 };
 
 // acc[r] = sum_j a_ij * V[col_j, lane columns] for the R rows of this row group.
@@ -506,27 +506,26 @@ __device__ __forceinline__ void spmm_slots(const Ctl& c, const Csr& A, const dou
       if (LPR < 32) maxlen = (int)__reduce_max_sync(FULL, (unsigned)maxlen);
       const int lim = any ? min(ln, CAP) : 0;  // entries gathered from registers
       const int inreg = min(maxlen, CAP);
+      // entry e sits in lane e % LPR, register slot e / LPR (compile-time per t)
 #pragma unroll
-      for (int q = 0; q < EPL; ++q) {
-        if (q * LPR >= inreg) break;
+      for (int b = 0; b < CAP; b += GB) {
+        if (b >= inreg) break;
+        double g[GB][CPL];
 #pragma unroll
-        for (int b = 0; b < LPR; b += GB) {
-          if (q * LPR + b >= inreg) break;
-          double g[GB][CPL];
+        for (int t = 0; t < GB; ++t) {
+          const int e = b + t;
+          if (e >= CAP) break;
+          const int cc = __shfl_sync(FULL, ci[e / LPR], e % LPR, LPR);
+          if (e < lim) gather_cols<CPL, NC>(Vl + (size_t)cc * KP, g[t]);
+        }
 #pragma unroll
-          for (int t = 0; t < GB; ++t) {
-            const int e = q * LPR + b + t;
-            const int cc = __shfl_sync(FULL, ci[q], (b + t) % LPR, LPR);
-            if (e < lim) gather_cols<CPL, NC>(Vl + (size_t)cc * KP, g[t]);
-          }
+        for (int t = 0; t < GB; ++t) {
+          const int e = b + t;
+          if (e >= CAP) break;
+          const double vv = __shfl_sync(FULL, cv[e / LPR], e % LPR, LPR);
+          if (e < lim) {
 #pragma unroll
-          for (int t = 0; t < GB; ++t) {
-            const int e = q * LPR + b + t;
-            const double vv = __shfl_sync(FULL, cv[q], (b + t) % LPR, LPR);
-            if (e < lim) {
-#pragma unroll
-              for (int k = 0; k < CPL; ++k) acc[k] = fma(vv, g[t][k], acc[k]);
-            }
+            for (int k = 0; k < CPL; ++k) acc[k] = fma(vv, g[t][k], acc[k]);
           }
         }
       }
@@ -1361,7 +1360,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
 // ---------------------------------------------------------------- host driver
 
 inline int grid_for(int n, int kp, int blocks_per_sm = BLOCKS_PER_SM) {
-  const int lpr = (kp >= 4) ? kp / 4 : kp / 2;
+  const int lpr = (kp >= 64) ? kp / 4 : kp / 2;  // Map<KP>::LPR
   const int rb = BLOCK / lpr;
   int g = sm_count() * blocks_per_sm;
   const int need = (n + rb - 1) / rb;
@@ -1385,7 +1384,7 @@ struct Layout {
 };
 
 inline int win_tile_rows(int kp) {  // Win<KP>::TR
-  const int lpr = (kp >= 4) ? kp / 4 : kp / 2;
+  const int lpr = (kp >= 64) ? kp / 4 : kp / 2;  // Map<KP>::LPR
   return WHALF / lpr;
 }
 
