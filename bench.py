@@ -119,7 +119,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- our arm
-def kernel_roofline(engine, A, rounds=20):
+def kernel_roofline(engine, A, rounds=20, config="c2"):
     """Per-kernel CUDA-event timing of a PCG round at the bench's batch width,
     algorithmic bytes per launch, fraction of the HBM peak."""
     import torch
@@ -164,7 +164,7 @@ def kernel_roofline(engine, A, rounds=20):
     if os.path.exists(tfile):
         try:
             with open(tfile) as f:
-                traffic = json.load(f).get(f"{dominant}<{kp}>")
+                traffic = json.load(f).get(config, {}).get(f"{dominant}<{kp}>")
         except Exception:
             traffic = None
     ach = kern[dominant]["gbs"]
@@ -295,7 +295,7 @@ def run_ours(args):
     A = None
     if rank == 0:
         A = engine.assemble()
-        roof = kernel_roofline(engine, A)
+        roof = kernel_roofline(engine, A, config=args.config)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         Ah = A.to_scipy()

@@ -73,6 +73,13 @@ const char* hf_last_error(void);
 int hf_device_sm_count(int32_t* sm_count);
 /* Kernels launched by this library so far (graph launches count their nodes). */
 long long hf_launch_count(void);
+/* Deterministic int32 exclusive scan of n counts into out (any n >= 0);
+ * *total (device int32) receives the sum.  This is the CSR row-pointer step
+ * (the cumsum inside scipy's coo -> csr conversion that fem.py:122-124 and
+ * meshgen.py:114-130 go through).  Scratch: hf_scan_workspace_bytes(n). */
+size_t hf_scan_workspace_bytes(int32_t n);
+int hf_exclusive_scan_i32(const int32_t* in, int32_t* out, int32_t n, int32_t* total, void* ws,
+                          size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------- solver */
 

@@ -51,8 +51,8 @@ __device__ __forceinline__ int32_t block_incl_scan(int32_t v, int32_t* sm) {
 }
 
 // Phase 1: per-tile exclusive scan, tile sums into bsum.
-__global__ void __launch_bounds__(SCAN_T) k_scan_tiles(const int32_t* __restrict__ in,
-                                                       int32_t* __restrict__ out, int n,
+// In-place safe (in == out): each thread reads its own elements before writing them.
+__global__ void __launch_bounds__(SCAN_T) k_scan_tiles(const int32_t* in, int32_t* out, int n,
                                                        int32_t* __restrict__ bsum) {
   __shared__ int32_t sm[32];
   const size_t base = (size_t)blockIdx.x * SCAN_TILE + threadIdx.x * SCAN_PER;
@@ -99,8 +99,14 @@ __global__ void k_scan_add(int32_t* out, int n, const int32_t* __restrict__ bsum
   if (i < (size_t)n) out[i] += bsum[i / SCAN_TILE];
 }
 
-size_t scan_scratch_elems(int32_t n) { return (size_t)(n + SCAN_TILE - 1) / SCAN_TILE + 32; }
+size_t scan_scratch_elems(int32_t n) {
+  const size_t nb = ((size_t)n + SCAN_TILE - 1) / SCAN_TILE;
+  return nb + (nb > (size_t)SCAN_TILE ? scan_scratch_elems((int32_t)nb) : 32);
+}
 
+// Exclusive scan of any int32 length: tile scan, recursive scan of the tile sums
+// (in place, next level's sums after them), then add-back.  Fixed order, so the
+// result is deterministic.
 int exclusive_scan_i32(const int32_t* in, int32_t* out, int32_t n, int32_t* block_sums,
                        int32_t* total_dev, cudaStream_t s) {
   if (n <= 0) {
@@ -108,14 +114,19 @@ int exclusive_scan_i32(const int32_t* in, int32_t* out, int32_t n, int32_t* bloc
     return HF_OK;
   }
   const int nb = (n + SCAN_TILE - 1) / SCAN_TILE;
-  if (nb > SCAN_TILE) {
-    set_error("scan: %d elements exceed the two-level limit", n);
-    return HF_ERR_ARG;
-  }
-  count_launches(nb > 1 ? 3 : 2);
+  count_launches(1);
   k_scan_tiles<<<nb, SCAN_T, 0, s>>>(in, out, n, block_sums);
-  k_scan_sums<<<1, SCAN_T, 0, s>>>(block_sums, nb, total_dev);
-  if (nb > 1) k_scan_add<<<(n + 255) / 256, 256, 0, s>>>(out, n, block_sums);
+  if (nb > SCAN_TILE) {
+    int rc = exclusive_scan_i32(block_sums, block_sums, nb, block_sums + nb, total_dev, s);
+    if (rc) return rc;
+  } else {
+    count_launches(1);
+    k_scan_sums<<<1, SCAN_T, 0, s>>>(block_sums, nb, total_dev);
+  }
+  if (nb > 1) {
+    count_launches(1);
+    k_scan_add<<<(n + 255) / 256, 256, 0, s>>>(out, n, block_sums);
+  }
   HF_LAUNCH_CHECK();
   return HF_OK;
 }
@@ -135,4 +146,22 @@ extern "C" int hf_device_sm_count(int32_t* out) {
   HF_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
   *out = v;
   return HF_OK;
+}
+
+extern "C" size_t hf_scan_workspace_bytes(int32_t n) {
+  return hf::scan_scratch_elems(n < 0 ? 0 : n) * sizeof(int32_t);
+}
+
+extern "C" int hf_exclusive_scan_i32(const int32_t* in, int32_t* out, int32_t n, int32_t* total,
+                                     void* ws, size_t ws_bytes, void* stream) {
+  if (n < 0 || !total || (n > 0 && (!in || !out || !ws))) {
+    hf::set_error("hf_exclusive_scan_i32: bad argument");
+    return HF_ERR_ARG;
+  }
+  if (ws_bytes < hf_scan_workspace_bytes(n)) {
+    hf::set_error("scan workspace too small");
+    return HF_ERR_WORKSPACE;
+  }
+  return hf::exclusive_scan_i32(in, out, n, reinterpret_cast<int32_t*>(ws), total,
+                                reinterpret_cast<cudaStream_t>(stream));
 }

@@ -139,3 +139,22 @@ def test_c1_pattern_hash(eng):
     assert sha(A.indptr.astype(np.int32)) == str(fx["A_sha_indptr"])
     assert sha(A.indices.astype(np.int32)) == str(fx["A_sha_indices"])
     _ = sp
+
+
+@pytest.mark.parametrize("n", [0, 1, 4095, 4096, 4097, 16_777_217, 40_000_003])
+def test_exclusive_scan_any_length(eng, n):
+    """CSR row-pointer scan: exact, including lengths past two tile levels (C5 has 28.7M elements)."""
+    import torch
+    from paper_1811_07717_b200 import _native as N
+
+    g = torch.Generator(device="cuda").manual_seed(n)
+    x = torch.randint(0, 4, (max(n, 1),), generator=g, device="cuda", dtype=torch.int32)[:n]
+    out = torch.empty_like(x)
+    tot = torch.zeros(1, dtype=torch.int32, device="cuda")
+    ws = torch.empty(max(N.lib.hf_scan_workspace_bytes(n), 1), dtype=torch.uint8, device="cuda")
+    N.check("hf_exclusive_scan_i32", N.lib.hf_exclusive_scan_i32(
+        N.ptr(x), N.ptr(out), n, N.ptr(tot), N.ptr(ws), ws.numel(), N.stream_handle()))
+    c = torch.cumsum(x.long(), 0)
+    assert int(tot.item()) == (int(c[-1]) if n else 0)
+    if n:
+        assert torch.equal(out.long(), c - x.long())

@@ -26,6 +26,6 @@ if args.build:
 else:
     import bench
 
-    print(bench.kernel_roofline(eng, A, rounds=args.rounds))
+    print(bench.kernel_roofline(eng, A, rounds=args.rounds, config=args.config))
 torch.cuda.synchronize()
 print("done")
