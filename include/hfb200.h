@@ -27,6 +27,7 @@
  *   hf_eit_sens            leadfield.py:179-207 _dof_sensitivities: Q[p,m,:] = T' K_m u_p
  *   hf_boundary_faces      meshgen.py:101-134  TetMesh.boundary_triangles
  *   hf_whitney_gt          fem.py:291-422      assemble_G (Whitney source matrix), as G'
+ *   hf_nearest_center      leadfield.py:96-99  build_dof_map: owner = argmin ||c_i - centre_j||
  *
  * See INTEGRATION.md for the ctypes binding the reference would use.
  */
@@ -221,6 +222,13 @@ int hf_whitney_gt(const double* nodes, const int32_t* tetra, int32_t n, int32_t 
                   const int32_t* src_elems, int32_t n_src, const double* orient, int32_t* gptr,
                   int32_t* gidx, double* gval, int64_t* nnz_out, void* ws, size_t ws_bytes,
                   void* stream);
+
+/* owner[i] = argmin_j ||points_i - centers_j|| (first index on ties) with the
+ * reference's arithmetic: sqrt((dx*dx + dy*dy) + dz*dz), each op rounded
+ * (build_dof_map, leadfield.py:96-99).  points (n_points x 3), centers
+ * (n_centers x 3) row-major fp64, owner int32; all device.  No workspace. */
+int hf_nearest_center(const double* points, int32_t n_points, const double* centers,
+                      int32_t n_centers, int32_t* owner, void* stream);
 
 #ifdef __cplusplus
 }

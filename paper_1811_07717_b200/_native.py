@@ -55,6 +55,7 @@ def _load():
         "hf_topology_workspace_bytes": (SZ, [I32, I32, I32]),
         "hf_boundary_faces": (C.c_int, [P, I32, I32, P, C.POINTER(I64), P, SZ, P]),
         "hf_whitney_gt": (C.c_int, [P, P, I32, I32, P, I32, P, P, P, P, C.POINTER(I64), P, SZ, P]),
+        "hf_nearest_center": (C.c_int, [P, I32, P, I32, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -72,7 +73,8 @@ EXPORTED = ("hf_version", "hf_last_error", "hf_device_sm_count", "hf_launch_coun
             "hf_pcg_workspace_bytes", "hf_pcg_multi", "hf_pcg_profile", "hf_p1_blocks",
             "hf_p1_assemble_workspace_bytes", "hf_p1_assemble_prepare", "hf_p1_assemble_fill",
             "hf_response_matrix", "hf_lf_tail", "hf_dense_lf", "hf_eit_sens",
-            "hf_topology_workspace_bytes", "hf_boundary_faces", "hf_whitney_gt")
+            "hf_topology_workspace_bytes", "hf_boundary_faces", "hf_whitney_gt",
+            "hf_nearest_center")
 
 
 class NativeError(RuntimeError):

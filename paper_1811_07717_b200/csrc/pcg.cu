@@ -518,10 +518,12 @@ __device__ __forceinline__ void spmm_slots(const Ctl& c, const Csr& A, const dou
           const int cc = __shfl_sync(FULL, ci[e / LPR], e % LPR, LPR);
           if (e < lim) gather_cols<CPL, NC>(Vl + (size_t)cc * KP, g[t]);
         }
+        // consume the batch last-issued first: the first FMA waits on the last
+        // gather, so the scheduler cannot start FMAs before every gather is issued
 #pragma unroll
-        for (int t = 0; t < GB; ++t) {
+        for (int t = GB - 1; t >= 0; --t) {
           const int e = b + t;
-          if (e >= CAP) break;
+          if (e >= CAP) continue;
           const double vv = __shfl_sync(FULL, cv[e / LPR], e % LPR, LPR);
           if (e < lim) {
 #pragma unroll

@@ -94,14 +94,27 @@ def _nearest_center_exact(cc, centers, chunk=8192):
     return owner
 
 
+def nearest_center_device(cc, centers):
+    """owner = argmin_j ||cc_i - centers_j|| on the GPU (hf_nearest_center):
+    the reference's rounding and first-index ties, every pair evaluated."""
+    dev = torch.device("cuda", torch.cuda.current_device())
+    P = torch.from_numpy(np.ascontiguousarray(cc, dtype=np.float64)).to(dev)
+    Cc = torch.from_numpy(np.ascontiguousarray(centers, dtype=np.float64)).to(dev)
+    owner = torch.empty(max(len(cc), 1), dtype=torch.int32, device=dev)
+    N.check("hf_nearest_center", N.lib.hf_nearest_center(
+        N.ptr(P), len(cc), N.ptr(Cc), len(centers), N.ptr(owner), N.stream_handle()))
+    return owner[: len(cc)].cpu().numpy().astype(np.int64)
+
+
 def build_dof_map(mesh, compartments, n_dofs, seed=0, chunk=8192, method="auto"):
     """Nearest-centre partition of the perturbable elements (leadfield.py:80-101).
 
     Same centre draw (rng.choice), same per-entry distance arithmetic and
-    first-index argmin as the reference.  Small problems run the reference's
-    dense comparison in element chunks; large ones (C4: 4.1M elements x 5,000
-    DOFs, where the reference needs a 459 GiB array) use an exact k-d-tree
-    search (`_nearest_center_exact`)."""
+    first-index argmin as the reference.  method: "device" (hf_nearest_center,
+    all pairs on the GPU; the default when CUDA is present), "tree" (exact
+    k-d-tree search on the host, `_nearest_center_exact`), "dense" (the
+    reference's comparison in element chunks).  C4 has 4.1M elements x 5,000
+    DOFs, where the reference needs a 459 GiB array."""
     cand = np.flatnonzero(np.isin(mesh.labels, np.asarray(compartments)))
     if cand.size == 0:
         raise DofError("no mesh elements in the perturbable compartments")
@@ -114,7 +127,12 @@ def build_dof_map(mesh, compartments, n_dofs, seed=0, chunk=8192, method="auto")
     centroids = mesh.centroids()
     centers = centroids[chosen]
     cc = centroids[cand]
-    if method == "tree" or (method == "auto" and len(cand) * n_dofs > 5e7):
+    if method == "auto":
+        method = "device" if torch.cuda.is_available() else (
+            "tree" if len(cand) * n_dofs > 5e7 else "dense")
+    if method == "device":
+        owner = nearest_center_device(cc, centers)
+    elif method == "tree":
         owner = _nearest_center_exact(cc, centers, chunk)
     else:
         owner = np.empty(len(cand), dtype=np.int64)

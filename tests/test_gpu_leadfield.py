@@ -132,3 +132,57 @@ def test_c1_leadfield_matches_reference(eng):
 
     _, info = solve_block(operator(A, cfg), rhs_block(sysm.B), cfg)
     assert np.all(np.abs(info.iterations - fx["iters"]) <= 1), (info.iterations, fx["iters"])
+
+
+def _dense_owner(cc, centers):
+    """The reference's owner computation (leadfield.py:98-99) in row chunks."""
+    out = []
+    for a in range(0, len(cc), 4096):
+        d = np.linalg.norm(cc[a:a + 4096][:, None, :] - centers[None, :, :], axis=2)
+        out.append(np.argmin(d, axis=1))
+    return np.concatenate(out)
+
+
+def test_dof_map_device_matches_reference(eng):
+    """build_dof_map on the GPU gives the reference's element sets (layered_h12 golden)."""
+    from paper_1811_07717_b200.leadfield import build_dof_map
+    from tests.fixtures import mesh_from_fixture
+
+    fx = load("layered_h12.npz")
+    mesh = mesh_from_fixture(fx)
+    dofs = build_dof_map(mesh, [0, 1], 20, seed=2, method="device")
+    np.testing.assert_array_equal(np.concatenate(dofs.element_sets), fx["eit_dof_elems"])
+    np.testing.assert_array_equal(np.cumsum([0] + [len(e) for e in dofs.element_sets]),
+                                  fx["eit_dof_ptr"])
+    np.testing.assert_array_equal(dofs.centers, fx["eit_centers"])
+
+
+@pytest.mark.parametrize("n_dofs", [1, 7, 500, 3000])
+def test_nearest_center_bitwise_argmin(eng, n_dofs):
+    """Every owner equals numpy's argmin of the reference's distance array (C1 mesh, 303k elements;
+    3000 centres span two shared-memory tiles)."""
+    from paper_1811_07717_b200.leadfield import nearest_center_device
+    from tests.fixtures import mesh_from_fixture
+
+    mesh = mesh_from_fixture(load("c1.npz"))
+    cc = mesh.centroids()
+    rng = np.random.default_rng(n_dofs)
+    centers = cc[rng.choice(len(cc), size=n_dofs, replace=False)]
+    sel = rng.choice(len(cc), size=40_000, replace=False)
+    np.testing.assert_array_equal(nearest_center_device(cc[sel], centers),
+                                  _dense_owner(cc[sel], centers))
+
+
+def test_nearest_center_ties_take_first_index(eng):
+    from paper_1811_07717_b200.leadfield import nearest_center_device
+
+    centers = np.array([[1.0, 0, 0], [-1.0, 0, 0], [1.0, 0, 0], [0, 3.0, 0]])
+    pts = np.array([[0.0, 0, 0], [0, 1.0, 0], [0, 0, 5.0], [2.0, 0, 0], [0, 3.0, 0]])
+    own = nearest_center_device(pts, centers)
+    np.testing.assert_array_equal(own, _dense_owner(pts, centers))
+    np.testing.assert_array_equal(own, [0, 0, 0, 0, 3])
+    # squares that differ by one ulp but share the rounded root keep the earlier centre
+    base = np.array([[0.0, 0.0, 0.0]])
+    s = 2.0
+    c2 = np.array([[np.sqrt(np.nextafter(s, 3)), 0, 0], [np.sqrt(s), 0, 0]])
+    np.testing.assert_array_equal(nearest_center_device(base, c2), _dense_owner(base, c2))
