@@ -184,10 +184,12 @@ int hf_lf_tail(const double* T, int32_t ldt, int32_t K, const hf_csr* Gt, const 
                int32_t L, int32_t ldw, double* LF, void* stream);
 
 /* Dense variant for the EIT Jacobian (leadfield.py:230-237):
- * out[l, c] = sum_k W[l,k] * Qc[c, k] for c < ncols, with Qc device ncols x L
- * row-major (i.e. out = W Qc').  out device L x ldo row-major. */
-int hf_dense_lf(const double* Qc, int32_t ncols, int32_t L, const double* W, double* out,
-                int32_t ldo, void* stream);
+ * out[l, c] = sum_{k<K} W[l*ldw + k] * Qc[c*K + k] for l < L, c < ncols, with Qc
+ * device ncols x K row-major (i.e. out = W[:, :K] Qc').  out device L x ldo
+ * row-major.  K = L for one device; K = the electrode block on a rank, with W
+ * pointing at the block's first column (distributed EIT partial sums). */
+int hf_dense_lf(const double* Qc, int32_t ncols, int32_t K, const double* W, int32_t L,
+                int32_t ldw, double* out, int32_t ldo, void* stream);
 
 /* EIT sensitivities Q[p, m, l] = sum_{e in dof m} sum_i T[conn_ei, l] (K_e u_e,p)_i
  * with unit-conductivity K_e whose ground rows/columns are zeroed

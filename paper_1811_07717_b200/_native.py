@@ -51,7 +51,7 @@ def _load():
         "hf_p1_assemble_fill": (C.c_int, [P, I32, I32, P, P, P, I32, I32, P, P, P, P, SZ, P]),
         "hf_response_matrix": (C.c_int, [pcsr, P, I32, I32, I32, I32, P, P, P]),
         "hf_lf_tail": (C.c_int, [P, I32, I32, pcsr, P, I32, I32, P, P]),
-        "hf_dense_lf": (C.c_int, [P, I32, I32, P, P, I32, P]),
+        "hf_dense_lf": (C.c_int, [P, I32, I32, P, I32, I32, P, I32, P]),
         "hf_eit_sens": (C.c_int, [P, P, P, P, I32, I32, P, I32, I32, P, I32, I32, P, P]),
         "hf_topology_workspace_bytes": (SZ, [I32, I32, I32]),
         "hf_boundary_faces": (C.c_int, [P, I32, I32, P, C.POINTER(I64), P, SZ, P]),

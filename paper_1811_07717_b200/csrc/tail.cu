@@ -269,13 +269,13 @@ extern "C" int hf_lf_tail(const double* T, int32_t ldt, int32_t K, const hf_csr*
                    reinterpret_cast<cudaStream_t>(stream));
 }
 
-extern "C" int hf_dense_lf(const double* Qc, int32_t ncols, int32_t L, const double* W,
-                           double* out, int32_t ldo, void* stream) {
+extern "C" int hf_dense_lf(const double* Qc, int32_t ncols, int32_t K, const double* W,
+                           int32_t L, int32_t ldw, double* out, int32_t ldo, void* stream) {
   if (!Qc || !W || !out || ldo < ncols) {
     set_error("hf_dense_lf: bad argument");
     return HF_ERR_ARG;
   }
-  return lf_launch(1, nullptr, 0, L, L, nullptr, Qc, ncols, W, L, out, ldo,
+  return lf_launch(1, nullptr, 0, L, K, nullptr, Qc, ncols, W, ldw, out, ldo,
                    reinterpret_cast<cudaStream_t>(stream));
 }
 

@@ -70,7 +70,9 @@ class EegEngine:
         self.Bt = DeviceCsr.from_scipy(sp.csr_matrix(sp.csr_matrix(B).T), dev)
         self.Cdiag = torch.from_numpy(np.ascontiguousarray(C.diagonal(), dtype=np.float64)).to(dev)
         self.R = np.asarray(R, dtype=np.float64)
-        if isinstance(G, DeviceCsr):  # already G' in HBM (topology.assemble_Gt_device)
+        if G is None:  # EIT: no source matrix
+            self.Gt, self.ncols = None, 0
+        elif isinstance(G, DeviceCsr):  # already G' in HBM (topology.assemble_Gt_device)
             self.Gt = G
             self.ncols = G.shape[0]
         elif hasattr(G, "element_ids"):  # a SourceSpace: assemble G' on the device
@@ -83,7 +85,11 @@ class EegEngine:
             Gs = G if sp.issparse(G) else sp.csr_matrix(np.asarray(G, dtype=float))
             self.Gt = DeviceCsr.from_scipy(sp.csr_matrix(Gs.T), dev)
             self.ncols = Gs.shape[1]
-        self.h2d_bytes += (Bc.nnz * 20 + self.Bt.nnz * 12 + self.Gt.nnz * 12 + 8 * self.L
+        self.mesh = mesh
+        self.B = sp.csr_matrix(B)
+        self._op = None
+        gnnz = self.Gt.nnz if self.Gt is not None else 0
+        self.h2d_bytes += (Bc.nnz * 20 + self.Bt.nnz * 12 + gnnz * 12 + 8 * self.L
                            + 4 * (self.n + 1) + 4 * (self.ncols + 1) + 4 * (self.L + 1))
         self.last_info = None
 
@@ -92,20 +98,43 @@ class EegEngine:
         blocks = blocks_device(self.dmesh, self.sigma, 0.0)
         return assemble_device(self.dmesh, blocks, self.n, self.etri, self.ecoef, self.ground)
 
+    def operator(self, A):
+        if self._op is None or self._op.A is not A:
+            op = PcgOperator(A, self.cfg.preconditioner)
+            if op.n_zero_rows:
+                from .errors import SingularPreconditionerError
+                raise SingularPreconditionerError(f"{op.n_zero_rows} zero row(s) in the operator")
+            self._op = op
+        return self._op
+
     def solve(self, A):
-        op = PcgOperator(A, self.cfg.preconditioner)
-        if op.n_zero_rows:
-            from .errors import SingularPreconditionerError
-            raise SingularPreconditionerError(f"{op.n_zero_rows} zero row(s) in the operator")
-        T, info = solve_block(op, self.Bd, self.cfg)
+        T, info = solve_block(self.operator(A), self.Bd, self.cfg)
         _raise_failed(info, T, self.cfg, column_tag=True)
         self.last_info = info
         return T
+
+    def solve_rhs(self, A, rhs):
+        """A^-1 rhs for a host n x k block with pcg_solve semantics (no column tag):
+        the EIT pattern solves u_p = A^-1 B M^-1 I_p (leadfield.py:223-227)."""
+        Rd = rhs_block(np.asarray(rhs, dtype=np.float64), dev=self.Bd.device)
+        U, info = solve_block(self.operator(A), Rd, self.cfg)
+        _raise_failed(info, U, self.cfg, column_tag=False)
+        return U
+
+    def eit_partial(self, dofs, T, U, W):
+        """This rank's share of the EIT Jacobian: W[:, block] Q_block[p]' stacked over
+        patterns (P*L x n_dofs), Q_block = T_block' K_m u_p (leadfield.py:179-207, 230-237)."""
+        from .leadfield import eit_columns_device
+
+        return eit_columns_device(self.mesh, dofs, self.ground, T, U, W, self.c0)
 
     def response_block(self, T):
         return response_block_device(self.Bt, T, self.L, self.Cdiag, self.c0)
 
     def lf_partial(self, T, W):
+        if self.Gt is None:
+            from .errors import SingularSystemError
+            raise SingularSystemError("no source matrix G on this engine")
         return lf_tail_device(T, self.Gt, np.ascontiguousarray(W[:, self.c0:self.c1]))
 
     # ---- single-rank build --------------------------------------------------

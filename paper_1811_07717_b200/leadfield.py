@@ -295,6 +295,24 @@ def dof_sensitivities_device(mesh, dofs, ground, T, U, L, P):
     return Q
 
 
+def eit_columns_device(mesh, dofs, ground, T, U, W, c0=0):
+    """EIT Jacobian columns cols[p*L:(p+1)*L] = W[:, c0:c0+k] Q[p]' (leadfield.py:230-237)
+    with Q = T' K_m u_p for the k transfer columns in T (electrodes c0..c0+k-1).
+    With every electrode (k = L) this is the lead field; on a rank holding an
+    electrode block it is that block's share of the sum over electrodes."""
+    L, k, P = W.shape[0], T.shape[1], U.shape[1]
+    dev = T.device
+    Q = dof_sensitivities_device(mesh, dofs, ground, T, U, k, P)      # P x nd x k
+    Wd = torch.from_numpy(np.ascontiguousarray(W)).to(dev)
+    nd = dofs.n_dofs
+    cols = torch.empty((P * L, nd), dtype=torch.float64, device=dev)
+    for p in range(P):
+        N.check("hf_dense_lf", N.lib.hf_dense_lf(
+            N.ptr(Q[p]), nd, k, N.ptr(Wd[:, c0:]), L, L, N.ptr(cols[p * L:(p + 1) * L]), nd,
+            N.stream_handle()))
+    return cols
+
+
 def eit_leadfield(sys, dofs, currents, cfg=PcgConfig(), threads=1):
     """Linearised EIT lead field around the mesh conductivity (leadfield.py:210-237)."""
     I = check_current_patterns(currents, sys.n_electrodes)
@@ -307,13 +325,7 @@ def eit_leadfield(sys, dofs, currents, cfg=PcgConfig(), threads=1):
     BV = dsys.Bd @ Vd                             # n x P right-hand sides u_p
     U, info = solve_block(dsys.op, BV, cfg)
     _raise_failed(info, U, cfg, column_tag=False)  # pcg_solve semantics: no column tag
-    Q = dof_sensitivities_device(sys.mesh, dofs, sys.ground, T, U, L, P)
-    W = torch.from_numpy(np.ascontiguousarray(response_operator(M, sys.R))).to(dev)
-    nd = dofs.n_dofs
-    cols = torch.empty((P * L, nd), dtype=torch.float64, device=dev)
-    for p in range(P):                            # cols[p-block] = W Q[p]'
-        N.check("hf_dense_lf", N.lib.hf_dense_lf(
-            N.ptr(Q[p]), nd, L, N.ptr(W), N.ptr(cols[p * L:(p + 1) * L]), nd, N.stream_handle()))
+    cols = eit_columns_device(sys.mesh, dofs, sys.ground, T, U, response_operator(M, sys.R))
     return LeadField(matrix=cols.cpu().numpy(), positions=dofs.centers, orientations=None,
                      modality="eit", n_patterns=P,
                      background_sigma=np.array(sys.mesh.sigma, copy=True),
@@ -322,5 +334,5 @@ def eit_leadfield(sys, dofs, currents, cfg=PcgConfig(), threads=1):
 
 __all__ = ["LeadField", "EitDofMap", "build_dof_map", "electrode_response", "eeg_leadfield",
            "check_current_patterns", "adjacent_pair_patterns", "eit_forward", "eit_leadfield",
-           "DeviceSystem", "lf_tail_device", "response_operator", "response_block_device",
+           "DeviceSystem", "lf_tail_device", "eit_columns_device", "response_operator", "response_block_device",
            "symmetrize"]

@@ -35,6 +35,10 @@ class OracleEngine:
         self.Cdiag = fx["Cdiag"]
         self.c0, self.c1 = columns
         self.cfg = oracle.PcgSettings(tolerance=float(fx["tol"]))
+        from tests.fixtures import mesh_from_fixture
+
+        self.mesh = mesh_from_fixture(fx)
+        self.ground = int(fx["ground"])
 
     def assemble(self):
         return self.A
@@ -52,6 +56,16 @@ class OracleEngine:
     def lf_partial(self, T, W):
         TtG = np.asarray((self.G.T @ T.numpy()).T)
         return torch.from_numpy(W[:, self.c0:self.c1] @ TtG)
+
+    # EIT stages (distributed.sharded_eit_leadfield)
+    def solve_rhs(self, A, rhs):
+        return torch.from_numpy(self.oracle.transfer_matrix(A, sp.csc_matrix(rhs), self.cfg))
+
+    def eit_partial(self, dofs, T, U, W):
+        Q = self.oracle.dof_sensitivities(self.mesh.nodes, self.mesh.tetra, dofs.element_sets,
+                                          self.ground, U.numpy(), T.numpy())
+        Wb = W[:, self.c0:self.c1]
+        return torch.from_numpy(np.concatenate([Wb @ Q[p].T for p in range(Q.shape[0])]))
 
 
 def _worker(rank, world, port, name, out):
@@ -88,3 +102,45 @@ def test_sharded_leadfield_gloo(tmp_path, world):
     assert np.linalg.norm(lf - ref) / np.linalg.norm(ref) <= 1e-6
     assert lf.shape == ref.shape
     _ = sp
+
+
+def _eit_worker(rank, world, port, name, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_1811_07717_b200.distributed import sharded_eit_leadfield
+    from paper_1811_07717_b200.engine import column_blocks
+    from paper_1811_07717_b200.leadfield import EitDofMap
+    from tests.fixtures import load
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fx = load(name)
+        L = int(fx["B_shape"][1])
+        eng = OracleEngine(fx, column_blocks(L, world)[rank])
+        dofs = EitDofMap(element_sets=tuple(np.split(fx["eit_dof_elems"], fx["eit_dof_ptr"][1:-1])),
+                         centers=fx["eit_centers"])
+        lf = sharded_eit_leadfield(eng, dofs, fx["eit_currents"], world, rank)
+        if rank == 0:
+            np.savez(out, m=lf.matrix, bg=lf.background_data, p=lf.n_patterns)
+        else:
+            assert lf is None
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_sharded_eit_leadfield_gloo(tmp_path, world):
+    """EIT over ranks: electrode-sharded T, pattern-sharded U + all-gather, summed Jacobian."""
+    from tests.fixtures import load
+
+    name = "layered_h12.npz"
+    out = str(tmp_path / "eit.npz")
+    mp.spawn(_eit_worker, args=(world, _free_port(), name, out), nprocs=world, join=True)
+    got = np.load(out)
+    fx = load(name)
+    ref = fx["eit_LF"]
+    assert got["m"].shape == ref.shape
+    assert np.linalg.norm(got["m"] - ref) / np.linalg.norm(ref) <= 1e-6
+    np.testing.assert_allclose(got["bg"], fx["eit_bg"], rtol=1e-8, atol=1e-14)
+    assert int(got["p"]) == fx["eit_currents"].shape[1]
