@@ -291,7 +291,10 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
 // The SpMM kernels are latency-bound gathers: they run one 512-thread block
 // per SM with a 128-register budget and keep R rows x GB gathers in flight
 // per lane group (all loads issued before any FMA consumes them).
-constexpr int GB = 8;  // gathers per batch
+#ifndef HF_GB
+#define HF_GB 8
+#endif
+constexpr int GB = HF_GB;  // gathers per batch
 
 template <int KP>
 struct Spmm {
