@@ -142,14 +142,16 @@ def kernel_roofline(engine, A, rounds=20, config="c2"):
         N.C.byref(op.Ac.struct), N.ptr(op.d), N.ptr(Bb), n, kp, rounds, N.ptr(X), ms,
         N.C.byref(fused), N.ptr(ws), ws.numel(), N.stream_handle()))
     nnz = op.Ac.nnz
-    if fused.value:
+    spmm = "k_spmm_ell" if fused.value & 2 else "k_spmm_pq"
+    if fused.value & 1:
         # k_xs: x/p update (read x, p, r, dd; write x, p) + next SpMM (write q; CSR);
         # the p rows it gathers were just written and are not re-read from DRAM
         algo = {"k_xs": 48 * n * kp + 12 * nnz + 4 * (n + 1) + 16 * n,
                 "k_update_r": 24 * n * kp + 16 * n}
         times = dict(zip(algo, [float(ms[0]), float(ms[1])]))
     else:
-        algo = {"k_spmm_pq": 16 * n * kp + 12 * nnz + 4 * (n + 1),
+        # the SpMM's algorithmic bytes count the CSR (the ELL copy reads 12 B x 8 slots per row)
+        algo = {spmm: 16 * n * kp + 12 * nnz + 4 * (n + 1),
                 "k_update_r": 24 * n * kp + 16 * n,
                 "k_update_xp": 40 * n * kp + 16 * n}
         times = dict(zip(algo, [float(ms[0]), float(ms[1]), float(ms[2])]))
@@ -173,7 +175,7 @@ def kernel_roofline(engine, A, rounds=20, config="c2"):
             "traffic": traffic, "algorithmic_bytes_per_launch": algo[dominant],
             "launch_ms": round(times[dominant], 4),
             "share_of_round": round(times[dominant] / total_ms, 3),
-            "pcg_round": {"kp": kp, "n": n, "nnz_spmm": nnz, "fused": bool(fused.value),
+            "pcg_round": {"kp": kp, "n": n, "nnz_spmm": nnz, "fused": bool(fused.value & 1),
                           "ms": round(total_ms, 4),
                           "bytes": total_bytes,
                           "gbs": round(total_bytes / (total_ms * 1e-3) / 1e9, 1),

@@ -120,8 +120,9 @@ int hf_pcg_multi(const hf_csr* A, const double* d, const double* B, int32_t n, i
 /* Timing probe for the roofline report: runs `rounds` PCG rounds of the same
  * kernels as hf_pcg_multi (tolerance 0, so no column stops) and writes the
  * average duration in ms, measured with CUDA events on `stream`, of
- * {k_spmm_pq, k_update_r, k_update_xp} or, when *fused (host int32) comes back
- * 1, of {k_xs, k_update_r, 0} (k_xs = x/p update fused with the next SpMM).
+ * {SpMM, k_update_r, k_update_xp} or, when bit 0 of *fused (host int32) is
+ * set, of {k_xs, k_update_r, 0} (k_xs = x/p update fused with the next SpMM).
+ * Bit 1 set: the SpMM is k_spmm_ell (ELL copy), else k_spmm_pq (CSR).
  * Same workspace as hf_pcg_multi. */
 int hf_pcg_profile(const hf_csr* A, const double* d, const double* B, int32_t n, int32_t kp,
                    int32_t rounds, double* X, float* ms3, int32_t* fused, void* ws,

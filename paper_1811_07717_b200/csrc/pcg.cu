@@ -144,26 +144,26 @@ __device__ __forceinline__ double zdiv(double x, double2 dd) {
 
 // Sum NV per-column values over the block in a fixed order and store the
 // block's partial row (KP values per quantity) at part[nv][blockIdx.x*KP].
-template <int KP, int NV>
-__device__ __forceinline__ void block_partials(double (&v)[NV][Map<KP>::CPL], double* sm,
-                                               double* part0, double* part1) {
-  using M = Map<KP>;
+// (lane g of a row group of LPR lanes holds columns g*CPL .. g*CPL+CPL-1)
+template <int KP, int NV, int CPL, int LPR>
+__device__ __forceinline__ void block_partials_map(double (&v)[NV][CPL], double* sm,
+                                                   double* part0, double* part1) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int glane = tid % M::LPR;
+  const int glane = tid % LPR;
 #pragma unroll
   for (int q = 0; q < NV; ++q)
 #pragma unroll
-    for (int c = 0; c < M::CPL; ++c) {
+    for (int c = 0; c < CPL; ++c) {
       double x = v[q][c];
 #pragma unroll
-      for (int off = 16; off >= M::LPR; off >>= 1) x += __shfl_xor_sync(FULL, x, off);
+      for (int off = 16; off >= LPR; off >>= 1) x += __shfl_xor_sync(FULL, x, off);
       v[q][c] = x;
     }
-  if (lane < M::LPR) {
+  if (lane < LPR) {
 #pragma unroll
     for (int q = 0; q < NV; ++q)
 #pragma unroll
-      for (int c = 0; c < M::CPL; ++c) sm[(q * NWARP + warp) * KP + glane * M::CPL + c] = v[q][c];
+      for (int c = 0; c < CPL; ++c) sm[(q * NWARP + warp) * KP + glane * CPL + c] = v[q][c];
   }
   __syncthreads();
   for (int col = tid; col < KP; col += BLOCK) {
@@ -174,6 +174,12 @@ __device__ __forceinline__ void block_partials(double (&v)[NV][Map<KP>::CPL], do
       (q == 0 ? part0 : part1)[(size_t)blockIdx.x * KP + col] = s;
     }
   }
+}
+
+template <int KP, int NV>
+__device__ __forceinline__ void block_partials(double (&v)[NV][Map<KP>::CPL], double* sm,
+                                               double* part0, double* part1) {
+  block_partials_map<KP, NV, Map<KP>::CPL, Map<KP>::LPR>(v, sm, part0, part1);
 }
 
 // Last-block detection; the last block reduces the partials of every block in
@@ -291,6 +297,7 @@ __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
 // The SpMM kernels are latency-bound gathers: they run one 512-thread block
 // per SM with a 128-register budget and keep R rows x GB gathers in flight
 // per lane group (all loads issued before any FMA consumes them).
+constexpr int ELL_W = 8;  // slots per row of the ELL SpMM copy (= the gather batch)
 #ifndef HF_GB
 #define HF_GB 8
 #endif
@@ -612,6 +619,178 @@ __global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
       if (act[k]) v[0][k] += p[k] * acc[k];
   });
   block_partials<KP, 1>(v, sm, c.part0, nullptr);
+  if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
+  if (tid < KP) {
+    if (s_act[tid]) c.alpha[tid] = c.rz[tid] / tot[tid];
+  }
+}
+
+// ---------------------------------------------------------------- SpMM over an ELL copy
+// k_spmm_ell: q = A p, p.q, alpha like k_spmm_pq, from an ELL copy of the
+// SpMM matrix (8 slots per row, built once per solve by k_ell_fill).  The row
+// pointers drop out of the dependency chain: a row's gathers wait on one
+// coalesced 8-slot load that is prefetched a step ahead.  Lanes own 2 columns
+// (128-bit gathers) and the kernel is register-light, so 32-48 warps/SM keep the
+// gathers in flight by occupancy instead of by register pipelining (a
+// microbenchmark of this shape on a C2-sized 7-point operator runs at 0.27 ms
+// vs 0.39 ms for the same gathers behind indptr -> indices).
+//   slot e < 8: (column, value), or (-1, 0) padding;  rows with more than 8
+//   entries keep entries 0..6 in slots 0..6 and put a marker (-2 - start, len)
+//   in slot 7; their entries 7.. are read from the CSR.
+// Sums run in spmm_slots' order (each batch of 8 entries last-first, then
+// entries 16.. in order), so q is bitwise that of k_spmm_pq / k_xs.
+#ifndef HF_ELL
+#define HF_ELL 1
+#endif
+#ifndef HF_ELL_HALF
+#define HF_ELL_HALF 0
+#endif
+#ifndef HF_ELL_BPS
+#define HF_ELL_BPS 2
+#endif
+template <int KP>
+struct Ell {
+  static constexpr int CPL = 2;
+  static constexpr int LPR = KP / CPL;    // lanes per row (8, 16, 32)
+  static constexpr int RB = BLOCK / LPR;  // rows per block step
+  static constexpr bool OK = (KP >= 16 && KP <= 64);
+};
+
+__global__ void k_ell_fill(int n, const int32_t* __restrict__ indptr,
+                           const int32_t* __restrict__ indices, const double* __restrict__ val,
+                           int* __restrict__ eci, double* __restrict__ ecv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int st = indptr[i], ln = indptr[i + 1] - st;
+  for (int e = 0; e < ELL_W; ++e) {
+    int c = -1;
+    double v = 0.0;
+    if (ln > ELL_W && e == ELL_W - 1) {
+      c = -2 - st;
+      v = (double)ln;
+    } else if (e < ln) {
+      c = indices[st + e];
+      v = val[st + e];
+    }
+    eci[(size_t)i * ELL_W + e] = c;
+    ecv[(size_t)i * ELL_W + e] = v;
+  }
+}
+
+template <int KP>
+__global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
+    k_spmm_ell(Ctl c, Csr A, const int* __restrict__ eci, const double* __restrict__ ecv,
+               const double* __restrict__ P, double* __restrict__ Q) {
+  using E = Ell<KP>;
+  constexpr int CPL = E::CPL, LPR = E::LPR, RB = E::RB;
+  __shared__ double sm[NWARP * KP > BLOCK ? NWARP * KP : BLOCK];
+  __shared__ double tot[KP];
+  __shared__ int s_act[KP];
+  if (c.summary[SUM_RUN] == 0) return;
+  const int tid = threadIdx.x, gl = tid % LPR;
+  for (int j = tid; j < KP; j += BLOCK) s_act[j] = (c.state[j] == S_RUN);
+  __syncthreads();
+  const bool act0 = s_act[gl * CPL] != 0, act1 = s_act[gl * CPL + 1] != 0;
+  const bool any = act0 || act1;
+  const int nt = (c.n + RB - 1) / RB;
+  const int slot = gl < ELL_W ? gl : ELL_W - 1;  // lane gl holds slot gl (lanes >= 8: unused copy)
+  auto row_at = [&](int t) {
+    const int r = t * RB + tid / LPR;
+    return (t < nt && r < c.n) ? r : -1;
+  };
+  auto load_slots = [&](int r, int& ci, double& cv) {
+    ci = -1;
+    cv = 0.0;
+    if (r >= 0) {
+      ci = __ldg(eci + (size_t)r * ELL_W + slot);
+      cv = __ldg(ecv + (size_t)r * ELL_W + slot);
+    }
+  };
+  const double* __restrict__ Pl = P + gl * CPL;
+  double v[1][CPL] = {{0.0, 0.0}};
+  int t = blockIdx.x;
+  int row = row_at(t), ci, ciN;
+  double cv, cvN;
+  load_slots(row, ci, cv);
+  for (; t < nt; t += c.G) {
+    const int rowN = row_at(t + c.G);
+    load_slots(rowN, ciN, cvN);  // next step's slots in flight during this one
+    // slots in batches of HB gathers, consumed last-first (slot 7 .. slot 0)
+    constexpr int HB = HF_ELL_HALF ? 4 : ELL_W, NBT = ELL_W / HB;
+    unsigned vm = 0;  // slots holding an entry
+    int c7 = -1, st = 0, ln = 0;
+    bool longrow = false;
+    double a0 = 0.0, a1 = 0.0;
+    const double cv7 = __shfl_sync(FULL, cv, ELL_W - 1, LPR);  // (outside divergent branches)
+#pragma unroll
+    for (int bt = NBT - 1; bt >= 0; --bt) {
+      double g[HB][CPL];
+#pragma unroll
+      for (int k = 0; k < HB; ++k) {
+        const int e = bt * HB + k;
+        const int cc = __shfl_sync(FULL, ci, e, LPR);
+        g[k][0] = g[k][1] = 0.0;
+        if (cc >= 0 && any) {
+          const double2 q2 = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)cc * KP));
+          g[k][0] = q2.x;
+          g[k][1] = q2.y;
+        }
+        vm |= (cc >= 0 && any) ? 1u << e : 0u;
+        if (e == ELL_W - 1) c7 = cc;
+      }
+      if (bt == NBT - 1) {
+        longrow = c7 < -1;
+        if (longrow) {  // entry 7 first (batch 0 runs last-first), from the CSR
+          st = -2 - c7;
+          ln = (int)cv7;
+          if (any) {
+            const int ce = __ldg(A.indices + st + 7);
+            const double ve = __ldg(A.val + st + 7);
+            const double2 q2 = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)ce * KP));
+            a0 = fma(ve, q2.x, a0);
+            a1 = fma(ve, q2.y, a1);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = HB - 1; k >= 0; --k) {
+        const int e = bt * HB + k;
+        const double vv = __shfl_sync(FULL, cv, e, LPR);
+        if ((vm >> e) & 1u) {
+          a0 = fma(vv, g[k][0], a0);
+          a1 = fma(vv, g[k][1], a1);
+        }
+      }
+    }
+    if (longrow && any) {  // entries 8..15 last-first, then 16.. in order
+      const int hi = min(ln, 16);
+      for (int e = hi - 1; e >= 8; --e) {
+        const int ce = __ldg(A.indices + st + e);
+        const double ve = __ldg(A.val + st + e);
+        const double2 q2 = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)ce * KP));
+        a0 = fma(ve, q2.x, a0);
+        a1 = fma(ve, q2.y, a1);
+      }
+      for (int e = 16; e < ln; ++e) {
+        const int ce = __ldg(A.indices + st + e);
+        const double ve = __ldg(A.val + st + e);
+        const double2 q2 = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)ce * KP));
+        a0 = fma(ve, q2.x, a0);
+        a1 = fma(ve, q2.y, a1);
+      }
+    }
+    if (any && row >= 0) {
+      const size_t o = (size_t)row * KP + gl * CPL;
+      *reinterpret_cast<double2*>(Q + o) = make_double2(a0, a1);
+      const double2 pr = __ldg(reinterpret_cast<const double2*>(P + o));  // L1: the diagonal's gather
+      if (act0) v[0][0] += pr.x * a0;
+      if (act1) v[0][1] += pr.y * a1;
+    }
+    row = rowN;
+    ci = ciN;
+    cv = cvN;
+  }
+  block_partials_map<KP, 1, CPL, LPR>(v, sm, c.part0, nullptr);
   if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
   if (tid < KP) {
     if (s_act[tid]) c.alpha[tid] = c.rz[tid] / tot[tid];
@@ -1385,6 +1564,8 @@ struct Layout {
   int4* tinfo;       // k_spmm_win tile windows
   int2* tranges;
   uint16_t* eslot;
+  int* ell_ci;     // k_spmm_ell: 8 slots per row (see k_ell_fill)
+  double* ell_cv;
   size_t bytes;
 };
 
@@ -1397,7 +1578,7 @@ inline Layout carve(void* ws, int n, int kp, int64_t nnz) {
   Carve cv{reinterpret_cast<char*>(ws), 0, ~size_t(0)};
   Layout L;
   const size_t nk = (size_t)n * kp;
-  const int gmax = sm_count() * BLOCKS_PER_SM;
+  const int gmax = sm_count() * 4;  // the most blocks any PCG kernel launches
   L.R = cv.take<double>(nk);
   L.P = cv.take<double>(nk);
   L.Q = cv.take<double>(nk);
@@ -1424,6 +1605,8 @@ inline Layout carve(void* ws, int n, int kp, int64_t nnz) {
   L.tinfo = cv.take<int4>(ntw + 1);
   L.tranges = cv.take<int2>((ntw + 1) * RCAP);
   L.eslot = cv.take<uint16_t>((size_t)nnz + 8);
+  L.ell_ci = cv.take<int>((size_t)n * ELL_W);
+  L.ell_cv = cv.take<double>((size_t)n * ELL_W);
   L.bytes = cv.used + 256;
   return L;
 }
@@ -1440,6 +1623,12 @@ __global__ void k_bandwidth(int n, const int32_t* __restrict__ indptr,
 // 128-register budget, its streaming half runs at 16 warps/SM and loses to
 // the three-kernel round (1.28 vs 1.00 ms at C2, kp=64).  Opt in with
 // HFB200_FUSED=1 while it is being reworked (warp-specialised x/p warps).
+// k_spmm_ell for kp 16..64 (default); HFB200_ELL=0 selects the CSR kernel k_spmm_pq.
+inline bool ell_enabled() {
+  const char* v = getenv("HFB200_ELL");
+  return HF_ELL && !(v && v[0] == '0');
+}
+
 inline bool fused_enabled() {
   const char* v = getenv("HFB200_FUSED");
   return v && v[0] == '1';
@@ -1458,7 +1647,7 @@ inline bool win_enabled() {
 
 template <int KP>
 int setup(const Layout& L, const hf_csr* A, int n, double tol, int max_iter, Ctl& c, Ctl& cs,
-          bool& fused, bool& win, cudaStream_t stream) {
+          Ctl& ce, bool& fused, bool& win, bool& ell, cudaStream_t stream) {
   memset(&c, 0, sizeof(c));
   c.n = n;
   c.kp = KP;
@@ -1502,7 +1691,38 @@ int setup(const Layout& L, const hf_csr* A, int n, double tol, int max_iter, Ctl
     cs.nb = (int)((nt + (long)cs.G * cs.tpb - 1) / ((long)cs.G * cs.tpb));
     HF_CUDA(cudaMemsetAsync(L.xdone, 0, sizeof(int) * (cs.nb + 1), stream));
   }
+  ce = cs;
+  ell = false;
+  if constexpr (Ell<KP>::OK) {
+    ell = !fused && !win && ell_enabled();
+    if (ell) {  // ELL copy of the SpMM matrix (once per solve)
+      const int nt = (n + Ell<KP>::RB - 1) / Ell<KP>::RB;
+      ce.G = std::max(1, std::min(sm_count() * HF_ELL_BPS, nt));
+      k_ell_fill<<<(n + 255) / 256, 256, 0, stream>>>(n, A->indptr, A->indices, A->val, L.ell_ci,
+                                                      L.ell_cv);
+      HF_LAUNCH_CHECK();
+      count_launches(1);
+    }
+  }
   return HF_OK;
+}
+
+// The unfused round's SpMM: the TMA-window, ELL or CSR kernel.
+template <int KP>
+inline void launch_round_spmm(const Ctl& cs, const Ctl& ce, const Csr& csr, const Layout& L,
+                              bool win, bool ell, cudaStream_t q) {
+  if (win) {
+    k_spmm_win<KP><<<cs.G, BLOCK, 4 * WIN_BYTES, q>>>(cs, csr, L.eslot, L.tinfo, L.tranges, L.P,
+                                                       L.Q, 0);
+    return;
+  }
+  if constexpr (Ell<KP>::OK) {
+    if (ell) {
+      k_spmm_ell<KP><<<ce.G, BLOCK, 0, q>>>(ce, csr, L.ell_ci, L.ell_cv, L.P, L.Q);
+      return;
+    }
+  }
+  k_spmm_pq<KP><<<cs.G, BLOCK, 0, q>>>(cs, csr, L.P, L.Q, 0);
 }
 
 template <int KP>
@@ -1529,14 +1749,15 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
     set_error("pcg workspace too small: need %zu, have %zu", L.bytes, ws_bytes);
     return HF_ERR_WORKSPACE;
   }
-  Ctl c, cs;
-  bool fused = false, win = false;
+  Ctl c, cs, ce;
+  bool fused = false, win = false, ell = false;
   Csr csr{A->indptr, A->indices, A->val};
-  if (int rc = setup<KP>(L, A, n, tol, max_iter, c, cs, fused, win, stream)) return rc;
+  if (int rc = setup<KP>(L, A, n, tol, max_iter, c, cs, ce, fused, win, ell, stream)) return rc;
   if (freeze_at != nullptr) {
     HF_CUDA(cudaMemcpyAsync(L.freeze, freeze_at, sizeof(int) * KP, cudaMemcpyDeviceToDevice, stream));
     c.freeze = L.freeze;
     cs.freeze = L.freeze;
+    ce.freeze = L.freeze;
   }
   HF_CUDA(cudaMemsetAsync(L.counter, 0, sizeof(unsigned int) * 4, stream));
   k_init<KP><<<c.G, BLOCK, 0, stream>>>(c, B, d, X, L.R, L.P);
@@ -1583,11 +1804,7 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
           cudaError_t e = launch_xs<KP>(cs, csr, X, L.P, L.R, L.Q, q);
           if (e != cudaSuccess) le = e;
         } else {
-          if (win)
-            k_spmm_win<KP><<<cs.G, BLOCK, 4 * WIN_BYTES, q>>>(cs, csr, L.eslot, L.tinfo, L.tranges,
-                                                               L.P, L.Q, 0);
-          else
-            k_spmm_pq<KP><<<cs.G, BLOCK, 0, q>>>(cs, csr, L.P, L.Q, 0);
+          launch_round_spmm<KP>(cs, ce, csr, L, win, ell, q);
           k_update_r<KP><<<c.G, BLOCK, 0, q>>>(c, L.Q, L.R);
           k_update_xp<KP><<<c.G, BLOCK, 0, q>>>(c, SUM_MASKED, X, L.P, L.R);
         }
@@ -1689,11 +1906,11 @@ int profile(const hf_csr* A, const double* d, const double* B, int n, int rounds
     set_error("pcg workspace too small");
     return HF_ERR_WORKSPACE;
   }
-  Ctl c, cs;
-  bool fused = false, win = false;
+  Ctl c, cs, ce;
+  bool fused = false, win = false, ell = false;
   Csr csr{A->indptr, A->indices, A->val};
-  if (int rc = setup<KP>(L, A, n, 0.0, 1 << 30, c, cs, fused, win, stream)) return rc;
-  *fused_out = fused ? 1 : 0;
+  if (int rc = setup<KP>(L, A, n, 0.0, 1 << 30, c, cs, ce, fused, win, ell, stream)) return rc;
+  *fused_out = (fused ? 1 : 0) | (ell ? 2 : 0);
   HF_CUDA(cudaMemsetAsync(L.counter, 0, sizeof(unsigned int) * 4, stream));
   k_init<KP><<<c.G, BLOCK, 0, stream>>>(c, B, d, X, L.R, L.P);
   if (fused) k_spmm_pq<KP><<<cs.G, BLOCK, 0, stream>>>(cs, csr, L.P, L.Q, 0);
@@ -1712,11 +1929,7 @@ int profile(const hf_csr* A, const double* d, const double* B, int n, int rounds
       cudaEventRecord(ev[3], stream);
     } else {
       cudaEventRecord(ev[0], stream);
-      if (win)
-        k_spmm_win<KP><<<cs.G, BLOCK, 4 * WIN_BYTES, stream>>>(cs, csr, L.eslot, L.tinfo,
-                                                               L.tranges, L.P, L.Q, 0);
-      else
-        k_spmm_pq<KP><<<cs.G, BLOCK, 0, stream>>>(cs, csr, L.P, L.Q, 0);
+      launch_round_spmm<KP>(cs, ce, csr, L, win, ell, stream);
       cudaEventRecord(ev[1], stream);
       k_update_r<KP><<<c.G, BLOCK, 0, stream>>>(c, L.Q, L.R);
       cudaEventRecord(ev[2], stream);

@@ -195,11 +195,41 @@ class TestTransferMatrix:
         A = csr(fx, "A")
         B = np.random.default_rng(5).normal(size=(A.shape[0], 40))
         B[fx["ground"]] = 0.0
+        monkeypatch.setenv("HFB200_ELL", "0")  # the CSR SpMM: same tiles and trees as k_xs
         monkeypatch.setenv("HFB200_FUSED", "0")
         T0 = eng.transfer_matrix(A, B)
         monkeypatch.setenv("HFB200_FUSED", "1")
         T1 = eng.transfer_matrix(A, B)
         np.testing.assert_array_equal(T0, T1)
+
+    @pytest.mark.parametrize("k", [16, 32, 64])
+    def test_ell_spmm_matches_csr(self, eng, monkeypatch, k):
+        """The ELL SpMM (default for kp 16..64) against the CSR one, on an SPD
+        matrix whose rows hold 1..20 entries (the > 8 entry rows take the
+        marker + CSR path): same solutions to the reduction-order rounding."""
+        import scipy.sparse as sp
+
+        rng = np.random.default_rng(k)
+        n = 3000
+        rows, cols = [], []
+        for i in range(n):
+            m = int(rng.choice([0, 1, 2, 3, 6, 9, 19], p=[.05, .2, .3, .2, .1, .1, .05]))
+            cc = rng.choice(n, size=m, replace=False)
+            rows += [i] * m
+            cols += list(cc)
+        M = sp.coo_matrix((rng.uniform(-1, 1, len(rows)), (rows, cols)), shape=(n, n)).tocsr()
+        M = M + M.T
+        A = (M + sp.diags(np.asarray(abs(M).sum(axis=1)).ravel() + 1.0)).tocsr()
+        lens = np.diff(A.indptr)
+        assert lens.max() > 16 and (lens <= 8).any()
+        B = rng.normal(size=(n, k))
+        cfg = eng.PcgConfig(tolerance=1e-12)
+        monkeypatch.setenv("HFB200_ELL", "0")
+        T0 = eng.transfer_matrix(A, B, cfg)
+        monkeypatch.setenv("HFB200_ELL", "1")
+        T1 = eng.transfer_matrix(A, B, cfg)
+        assert np.linalg.norm(T1 - T0) / np.linalg.norm(T0) < 1e-10
+        assert np.linalg.norm(A @ T1 - B) / np.linalg.norm(B) < 1e-11
 
     def test_tma_window_spmm_matches(self, eng, monkeypatch):
         """The TMA-windowed SpMM (HFB200_WIN=1) sums the same entries in the
