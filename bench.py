@@ -119,7 +119,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- our arm
-def kernel_roofline(engine, A, rounds=20, config="c2"):
+def kernel_roofline(engine, A, rounds=24, config="c2"):
     """Per-kernel CUDA-event timing of a PCG round at the bench's batch width,
     algorithmic bytes per launch, fraction of the HBM peak."""
     import torch
@@ -151,9 +151,17 @@ def kernel_roofline(engine, A, rounds=20, config="c2"):
         times = dict(zip(algo, [float(ms[0]), float(ms[1])]))
     else:
         # the SpMM's algorithmic bytes count the CSR (the ELL copy reads 12 B x 8 slots per row)
+        xd = fused.value >> 8
+        if xd > 1:
+            # x deferred over a ring of xd p blocks: xd-1 p-only rounds (read p, r;
+            # write p) and one x round (x read+write, xd p reads, r read, p write),
+            # averaged per round; dd (16 B/row) read in every round
+            upd = ("k_update_pxring", ((xd - 1) * 24 + 32 + 8 * xd) * n * kp // xd + 16 * n)
+        else:
+            upd = ("k_update_xp", 40 * n * kp + 16 * n)
         algo = {spmm: 16 * n * kp + 12 * nnz + 4 * (n + 1),
                 "k_update_r": 24 * n * kp + 16 * n,
-                "k_update_xp": 40 * n * kp + 16 * n}
+                upd[0]: upd[1]}
         times = dict(zip(algo, [float(ms[0]), float(ms[1]), float(ms[2])]))
     peak, peak_kind = peaks()
     kern = {name: {"ms": times[name], "bytes": algo[name],
@@ -176,6 +184,7 @@ def kernel_roofline(engine, A, rounds=20, config="c2"):
             "launch_ms": round(times[dominant], 4),
             "share_of_round": round(times[dominant] / total_ms, 3),
             "pcg_round": {"kp": kp, "n": n, "nnz_spmm": nnz, "fused": bool(fused.value & 1),
+                          "x_deferral": max(1, fused.value >> 8),
                           "ms": round(total_ms, 4),
                           "bytes": total_bytes,
                           "gbs": round(total_bytes / (total_ms * 1e-3) / 1e9, 1),

@@ -258,3 +258,46 @@ class TestTransferMatrix:
         _, info = solve_block(op, rhs_block(csr(fx, "B")), cfg)
         assert np.all(np.abs(info.iterations - fx["iters"]) <= 1), (info.iterations, fx["iters"])
         assert np.all(info.true_residual <= cfg.tolerance)
+
+    @pytest.mark.parametrize("k", [3, 16, 40, 70])
+    def test_deferred_x_is_bit_identical(self, eng, monkeypatch, k):
+        """x deferred over the ring of XD p blocks (default) replays the same
+        x += alpha p roundings as one x update per round (HFB200_XDEFER=0):
+        solutions, iteration counts and residuals are bitwise equal, including
+        columns that converge mid-chunk and residual replacements (tol 1e-13)."""
+        from paper_1811_07717_b200.solver import operator, rhs_block, solve_block
+        from tests.fixtures import csr
+
+        fx = load("layered_h14_tensor.npz")
+        A = csr(fx, "A")
+        B = np.random.default_rng(10 + k).normal(size=(A.shape[0], k))
+        B[fx["ground"]] = 0.0
+        B[:, k // 2] = 0.0  # a zero column rides along
+        out = {}
+        for flag in ("0", "1"):
+            monkeypatch.setenv("HFB200_XDEFER", flag)
+            for tol in (1e-8, 1e-13):
+                cfg = eng.PcgConfig(tolerance=tol)
+                X, info = solve_block(operator(A, cfg), rhs_block(B), cfg)
+                out[flag, tol] = (X.cpu().numpy(), info)
+        for tol in (1e-8, 1e-13):
+            X0, i0 = out["0", tol]
+            X1, i1 = out["1", tol]
+            np.testing.assert_array_equal(X0, X1)
+            np.testing.assert_array_equal(i0.iterations, i1.iterations)
+            np.testing.assert_array_equal(i0.true_residual, i1.true_residual)
+
+    def test_deferred_x_best_iterate(self, eng, monkeypatch):
+        """A failing column's best iterate (replayed to best_iter) is the same
+        with and without deferred x."""
+        A = sp.csr_matrix(random_spd(60, seed=3, cond=1e8))
+        B = np.random.default_rng(3).normal(size=(60, 5))
+        cfg = eng.PcgConfig(tolerance=1e-15, max_iterations=13)
+        got = []
+        for flag in ("0", "1"):
+            monkeypatch.setenv("HFB200_XDEFER", flag)
+            with pytest.raises(eng.ConvergenceError) as exc:
+                eng.transfer_matrix(A, B, cfg)
+            got.append(exc.value)
+        np.testing.assert_array_equal(got[0].best_x, got[1].best_x)
+        assert got[0].column == got[1].column and got[0].residual == got[1].residual
