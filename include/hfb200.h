@@ -28,6 +28,10 @@
  *   hf_boundary_faces      meshgen.py:101-134  TetMesh.boundary_triangles
  *   hf_whitney_gt          fem.py:291-422      assemble_G (Whitney source matrix), as G'
  *   hf_nearest_center      leadfield.py:96-99  build_dof_map: owner = argmin ||c_i - centre_j||
+ *   hf_locate              geometry.py:147-374 Segmentation.locate (ray-parity point location)
+ *   hf_grid_tets           meshgen.py:205-223  generate_mesh's Kuhn grid + element centroids
+ *   hf_mesh_compact        meshgen.py:224-235  keep labelled elements, np.unique node renumbering
+ *   hf_apply_priorities    meshgen.py:247-269  _apply_priorities
  *
  * See INTEGRATION.md for the ctypes binding the reference would use.
  */
@@ -232,6 +236,54 @@ int hf_whitney_gt(const double* nodes, const int32_t* tetra, int32_t n, int32_t 
  * (n_centers x 3) row-major fp64, owner int32; all device.  No workspace. */
 int hf_nearest_center(const double* points, int32_t n_points, const double* centers,
                       int32_t n_centers, int32_t* owner, void* stream);
+
+/* ---------------------------------------------------------------- mesh generation (next row #4, §8f) */
+
+/* A segmentation for hf_locate (geometry.py:317-374): compartments innermost
+ * first, each a union of closed surfaces.  All arrays device.
+ *   comp_surf  n_comp+1   surfaces of compartment k: comp_surf[k] .. comp_surf[k+1]-1
+ *   tri_off    n_surf+1   triangles of surface s: tri_off[s] .. tri_off[s+1]-1
+ *   box        n_surf x 8 {lo.x, lo.y, lo.z, hi.x, hi.y, hi.z, tol, 0}, tol = 1e-9 * diameter
+ *   rays       16 doubles per (surface, direction, triangle), surface s's block at row
+ *              tri_off[s] * n_dir, direction d at + d * n_tri(s): {h(3), k(3), n(3), c_h, c_k,
+ *              c_n, f, parallel (1/0), tol * 2 * area, 0} exactly as SurfaceMesh._cast
+ *              derives them for direction d (geometry.py:203-224). */
+typedef struct {
+  int32_t n_comp, n_surf, n_dir;
+  const int32_t* comp_surf;
+  const int32_t* tri_off;
+  const double* box;
+  const double* rays;
+} hf_segmentation;
+
+/* labels[i] = innermost compartment containing points[i] (on-surface counts as
+ * inside), -1 outside all (Segmentation.locate, geometry.py:359-374).
+ * points device n x 3 fp64, labels device int32.  No workspace. */
+int hf_locate(const hf_segmentation* seg, const double* points, int32_t n_points, int32_t* labels,
+              void* stream);
+
+/* generate_mesh's grid (meshgen.py:205-223): nx*ny*nz cubes, cx fastest, 6 Kuhn
+ * tetrahedra per cube in _KUHN_TETS order; tetra (device 6*ncube x 4 int32) holds
+ * grid node ids ix + (nx+1)(iy + (ny+1) iz), centroids (device 6*ncube x 3) the
+ * corner means.  xs/ys/zs (device, nx+1 / ny+1 / nz+1) are the grid coordinates. */
+int hf_grid_tets(const double* xs, const double* ys, const double* zs, int32_t nx, int32_t ny,
+                 int32_t nz, int32_t* tetra, double* centroids, void* stream);
+
+/* Keep the elements with label >= 0 in order, number the used grid nodes
+ * ascending and renumber the corners (the np.unique(return_inverse) of
+ * meshgen.py:229-232).  tetra_out (capacity m_all x 4), labels_out (m_all),
+ * nodes_out (capacity (nx+1)(ny+1)(nz+1) x 3) device; *m_out, *n_out host.
+ * ws: hf_mesh_compact_workspace_bytes(m_all, (nx+1)(ny+1)(nz+1)). */
+size_t hf_mesh_compact_workspace_bytes(int32_t m_all, int32_t n_grid);
+int hf_mesh_compact(const int32_t* tetra_all, const int32_t* cent_label, int32_t m_all,
+                    const double* xs, const double* ys, const double* zs, int32_t nx, int32_t ny,
+                    int32_t nz, int32_t* tetra_out, int32_t* labels_out, double* nodes_out,
+                    int64_t* m_out, int64_t* n_out, void* ws, size_t ws_bytes, void* stream);
+
+/* _apply_priorities (meshgen.py:247-269) in place on labels (device m), from the
+ * node labels (device n) and the compartment priorities (device n_comp). */
+int hf_apply_priorities(const int32_t* tetra, int32_t m, const int32_t* node_label,
+                        const int32_t* priority, int32_t* labels, void* stream);
 
 #ifdef __cplusplus
 }

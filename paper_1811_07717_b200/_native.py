@@ -23,6 +23,12 @@ class HfCsr(C.Structure):
                 ("indptr", C.c_void_p), ("indices", C.c_void_p), ("val", C.c_void_p)]
 
 
+class HfSegmentation(C.Structure):
+    _fields_ = [("n_comp", C.c_int32), ("n_surf", C.c_int32), ("n_dir", C.c_int32),
+                ("comp_surf", C.c_void_p), ("tri_off", C.c_void_p), ("box", C.c_void_p),
+                ("rays", C.c_void_p)]
+
+
 def _load():
     if not os.path.exists(LIB_PATH):
         raise ImportError(
@@ -57,6 +63,12 @@ def _load():
         "hf_boundary_faces": (C.c_int, [P, I32, I32, P, C.POINTER(I64), P, SZ, P]),
         "hf_whitney_gt": (C.c_int, [P, P, I32, I32, P, I32, P, P, P, P, C.POINTER(I64), P, SZ, P]),
         "hf_nearest_center": (C.c_int, [P, I32, P, I32, P, P]),
+        "hf_locate": (C.c_int, [C.POINTER(HfSegmentation), P, I32, P, P]),
+        "hf_grid_tets": (C.c_int, [P, P, P, I32, I32, I32, P, P, P]),
+        "hf_mesh_compact_workspace_bytes": (SZ, [I32, I32]),
+        "hf_mesh_compact": (C.c_int, [P, P, I32, P, P, P, I32, I32, I32, P, P, P, C.POINTER(I64),
+                                      C.POINTER(I64), P, SZ, P]),
+        "hf_apply_priorities": (C.c_int, [P, I32, P, P, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -75,7 +87,8 @@ EXPORTED = ("hf_version", "hf_last_error", "hf_device_sm_count", "hf_launch_coun
             "hf_p1_assemble_workspace_bytes", "hf_p1_assemble_prepare", "hf_p1_assemble_fill",
             "hf_response_matrix", "hf_lf_tail", "hf_dense_lf", "hf_eit_sens",
             "hf_topology_workspace_bytes", "hf_boundary_faces", "hf_whitney_gt",
-            "hf_nearest_center")
+            "hf_nearest_center", "hf_locate", "hf_grid_tets", "hf_mesh_compact_workspace_bytes",
+            "hf_mesh_compact", "hf_apply_priorities")
 
 
 class NativeError(RuntimeError):

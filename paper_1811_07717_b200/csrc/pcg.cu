@@ -671,6 +671,23 @@ __global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
 #ifndef HF_ELL_BPS
 #define HF_ELL_BPS 2
 #endif
+// HF_ELL_CT: tiles per chunk.  1 = tiles dealt round-robin (tile t -> block
+// t % G).  > 1: a block sweeps CT consecutive tiles before the grid moves on,
+// so the rows a gather reaches within the same x-line / y-neighbour line are
+// re-read from L1 instead of L2 (the grid still sweeps the mesh as one band of
+// G*CT tiles, which keeps the z-plane neighbours in L2).
+#ifndef HF_ELL_CT
+#define HF_ELL_CT 1
+#endif
+// HF_ELL_FAR: gathers of rows farther than this from the output row (the
+// z-plane neighbours of a grid-ordered mesh, used once per SM) skip L1
+// allocation so they do not evict the near rows (0: off).
+#ifndef HF_ELL_FAR
+#define HF_ELL_FAR 0
+#endif
+#ifndef HF_ELL_BCAST
+#define HF_ELL_BCAST 0
+#endif
 template <int KP>
 struct Ell {
   static constexpr int CPL = 2;
@@ -731,12 +748,95 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
   };
   const double* __restrict__ Pl = P + gl * CPL;
   double v[1][CPL] = {{0.0, 0.0}};
-  int t = blockIdx.x;
+  // slot s of this block -> tile (chunks of HF_ELL_CT consecutive tiles, dealt round-robin)
+  auto tile_of = [&](int s) {
+    if constexpr (HF_ELL_CT == 1) return (int)blockIdx.x + s * c.G;
+    else return ((s / HF_ELL_CT) * c.G + (int)blockIdx.x) * HF_ELL_CT + s % HF_ELL_CT;
+  };
+  auto gather2 = [&](int cc, int r, double2& q2) {
+    const double* gp = Pl + (size_t)cc * KP;
+    if (HF_ELL_FAR > 0 && abs(cc - r) > HF_ELL_FAR) {
+      asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(q2.x), "=d"(q2.y) : "l"(gp));
+    } else {
+      q2 = __ldg(reinterpret_cast<const double2*>(gp));
+    }
+  };
+#if HF_ELL_BCAST
+  // Every lane of a row group loads the row's 8 (column, value) slots itself
+  // (same-address loads: one L1 wavefront per 16 bytes for the whole row group)
+  // instead of receiving them by 16 shuffles: the L1 data pipe, which carries
+  // both, is this kernel's busiest unit (82% at C2).  Values are loaded after the
+  // gathers are issued, so their latency hides under the gathers'.
+  auto load_ci = [&](int r, int4& x0, int4& x1) {
+    if (r >= 0) {
+      x0 = __ldg(reinterpret_cast<const int4*>(eci + (size_t)r * ELL_W));
+      x1 = __ldg(reinterpret_cast<const int4*>(eci + (size_t)r * ELL_W) + 1);
+    } else {
+      x0 = x1 = make_int4(-1, -1, -1, -1);
+    }
+  };
+  int s = 0, t = tile_of(0);
+  int row = row_at(t);
+#if HF_ELL_BCAST == 2
+  for (; t < nt; t = tile_of(++s)) {  // slots of the next row prefetched into L1, not registers
+    const int rowN = row_at(tile_of(s + 1));
+    if (rowN >= 0 && gl == 0) {
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(eci + (size_t)rowN * ELL_W));
+      asm volatile("prefetch.global.L1 [%0];" ::"l"(ecv + (size_t)rowN * ELL_W));
+    }
+    int4 c0, c1;
+    load_ci(row, c0, c1);
+#else
+  int4 c0, c1;
+  load_ci(row, c0, c1);
+  for (; t < nt; t = tile_of(++s)) {
+    const int rowN = row_at(tile_of(s + 1));
+    int4 n0, n1;
+    load_ci(rowN, n0, n1);  // next step's columns in flight during this one
+#endif
+    const int cc[ELL_W] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    double g[ELL_W][CPL];
+#pragma unroll
+    for (int e = 0; e < ELL_W; ++e) {
+      g[e][0] = g[e][1] = 0.0;
+      if (cc[e] >= 0 && any) {
+        double2 q2;
+        gather2(cc[e], row, q2);
+        g[e][0] = q2.x;
+        g[e][1] = q2.y;
+      }
+    }
+    double a0 = 0.0, a1 = 0.0;
+    const bool longrow = cc[ELL_W - 1] < -1;
+    int st = 0, ln = 0;
+    if (row >= 0 && any) {
+      const double2* vp = reinterpret_cast<const double2*>(ecv + (size_t)row * ELL_W);
+      const double2 v01 = __ldg(vp), v23 = __ldg(vp + 1), v45 = __ldg(vp + 2), v67 = __ldg(vp + 3);
+      const double vv[ELL_W] = {v01.x, v01.y, v23.x, v23.y, v45.x, v45.y, v67.x, v67.y};
+      if (longrow) {  // entry 7 first (the batch runs last-first), from the CSR
+        st = -2 - cc[ELL_W - 1];
+        ln = (int)vv[ELL_W - 1];
+        const int ce = __ldg(A.indices + st + 7);
+        const double ve = __ldg(A.val + st + 7);
+        const double2 q2 = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)ce * KP));
+        a0 = fma(ve, q2.x, a0);
+        a1 = fma(ve, q2.y, a1);
+      }
+#pragma unroll
+      for (int e = ELL_W - 1; e >= 0; --e) {
+        if (cc[e] >= 0) {
+          a0 = fma(vv[e], g[e][0], a0);
+          a1 = fma(vv[e], g[e][1], a1);
+        }
+      }
+    }
+#else
+  int s = 0, t = tile_of(0);
   int row = row_at(t), ci, ciN;
   double cv, cvN;
   load_slots(row, ci, cv);
-  for (; t < nt; t += c.G) {
-    const int rowN = row_at(t + c.G);
+  for (; t < nt; t = tile_of(++s)) {
+    const int rowN = row_at(tile_of(s + 1));
     load_slots(rowN, ciN, cvN);  // next step's slots in flight during this one
     // slots in batches of HB gathers, consumed last-first (slot 7 .. slot 0)
     constexpr int HB = HF_ELL_HALF ? 4 : ELL_W, NBT = ELL_W / HB;
@@ -754,7 +854,8 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
         const int cc = __shfl_sync(FULL, ci, e, LPR);
         g[k][0] = g[k][1] = 0.0;
         if (cc >= 0 && any) {
-          const double2 q2 = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)cc * KP));
+          double2 q2;
+          gather2(cc, row, q2);
           g[k][0] = q2.x;
           g[k][1] = q2.y;
         }
@@ -785,6 +886,7 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
         }
       }
     }
+#endif
     if (longrow && any) {  // entries 8..15 last-first, then 16.. in order
       const int hi = min(ln, 16);
       for (int e = hi - 1; e >= 8; --e) {
@@ -810,8 +912,13 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
       if (act1) v[0][1] += pr.y * a1;
     }
     row = rowN;
+#if HF_ELL_BCAST == 1
+    c0 = n0;
+    c1 = n1;
+#elif HF_ELL_BCAST == 0
     ci = ciN;
     cv = cvN;
+#endif
   }
   block_partials_map<KP, 1, CPL, LPR>(v, sm, c.part0, nullptr);
   if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
@@ -1917,7 +2024,7 @@ int setup(const Layout& L, const hf_csr* A, int n, double tol, int max_iter, Ctl
     ell = !fused && !win && ell_enabled();
     if (ell) {  // ELL copy of the SpMM matrix (once per solve)
       const int nt = (n + Ell<KP>::RB - 1) / Ell<KP>::RB;
-      ce.G = std::max(1, std::min(sm_count() * HF_ELL_BPS, nt));
+      ce.G = std::max(1, std::min(sm_count() * HF_ELL_BPS, (nt + HF_ELL_CT - 1) / HF_ELL_CT));
       k_ell_fill<<<(n + 255) / 256, 256, 0, stream>>>(n, A->indptr, A->indices, A->val, L.ell_ci,
                                                       L.ell_cv);
       HF_LAUNCH_CHECK();

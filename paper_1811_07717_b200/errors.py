@@ -16,12 +16,15 @@ try:  # pragma: no cover - depends on the environment
         CurrentPatternError,
         DofError,
         ElectrodeError,
+        EmptyMeshError,
+        FormatError,
         HeadfemError,
         LocationError,
         ParameterError,
         SetupError,
         SingularPreconditionerError,
         SingularSystemError,
+        TopologyError,
     )
     FROM_REFERENCE = True
 except ImportError:
@@ -35,6 +38,15 @@ except ImportError:
 
     class ComputationError(HeadfemError):
         """Numerical or runtime failure (CLI exit code 3)."""
+
+    class FormatError(SetupError):
+        """Malformed input data (errors.py:24)."""
+
+    class TopologyError(SetupError):
+        """A surface is not closed or not consistently oriented (errors.py:28)."""
+
+    class EmptyMeshError(ComputationError):
+        """Mesh generation produced no elements (errors.py:34)."""
 
     class ParameterError(SetupError):
         """A numeric parameter is outside its admissible range."""
@@ -75,6 +87,6 @@ except ImportError:
 
 __all__ = [
     "HeadfemError", "SetupError", "ComputationError", "ParameterError", "AssemblyError",
-    "ElectrodeError", "LocationError", "SingularPreconditionerError", "ConvergenceError",
+    "ElectrodeError", "LocationError", "FormatError", "TopologyError", "EmptyMeshError", "SingularPreconditionerError", "ConvergenceError",
     "SingularSystemError", "CurrentPatternError", "DofError", "FROM_REFERENCE",
 ]

@@ -45,3 +45,23 @@ def system_from_fixture(fx, use_reference_A=True):
     sysm = model.CemSystem(mesh=mesh, electrodes=el, A=A, B=B, C=C, R=R,
                            ground=int(fx["ground"]), G=G, source_space=src)
     return mesh, el, sysm, src
+
+
+def seg_parts(fx, key):
+    """[(surfaces [(nodes, tris)], conductivity, priority)] of a stored segmentation."""
+    out = []
+    for c in range(int(fx[f"{key}_ncomp"])):
+        surfs = [(fx[f"{key}_c{c}_s{s}_nodes"], fx[f"{key}_c{c}_s{s}_tris"])
+                 for s in range(int(fx[f"{key}_c{c}_nsurf"]))]
+        cond = fx[f"{key}_c{c}_cond"]
+        out.append((surfs, float(cond[0]) if cond.size == 1 else cond, int(fx[f"{key}_c{c}_prio"])))
+    return out
+
+
+def segmentation(fx, key):
+    """The stored segmentation as the package's geometry mirror types."""
+    from paper_1811_07717_b200 import geometry as G
+
+    return G.Segmentation([G.Compartment([G.SurfaceMesh(nd, tr) for nd, tr in surfs], cond,
+                                         priority=pri)
+                           for surfs, cond, pri in seg_parts(fx, key)])
