@@ -688,6 +688,9 @@ __global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
 #ifndef HF_ELL_BCAST
 #define HF_ELL_BCAST 0
 #endif
+#ifndef HF_ELL_SMEM
+#define HF_ELL_SMEM 1
+#endif
 template <int KP>
 struct Ell {
   static constexpr int CPL = 2;
@@ -761,7 +764,74 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
       q2 = __ldg(reinterpret_cast<const double2*>(gp));
     }
   };
-#if HF_ELL_BCAST
+#if HF_ELL_SMEM
+  // The row's 8 (column, value) slots reach every lane of its row group through
+  // a per-group shared-memory slot (lanes 0..7 store them, then LDS.128
+  // broadcasts) instead of 26 SHFL.32 (a double shuffles as two): the L1 data
+  // pipe carries both and is this kernel's busiest unit (82% at C2), and the
+  // broadcast reads cost 6 wavefronts per row instead of 26.  Slots of the next
+  // row stay prefetched in registers (lanes 0..7), buffers alternate by step.
+  __shared__ __align__(16) int s_ci[2][RB][ELL_W];
+  __shared__ __align__(16) double s_cv[2][RB][ELL_W];
+  const int grp = tid / LPR;
+  int s = 0, t = tile_of(0);
+  int row = row_at(t), ci, ciN;
+  double cv, cvN;
+  load_slots(row, ci, cv);
+  for (; t < nt; t = tile_of(++s)) {
+    const int rowN = row_at(tile_of(s + 1));
+    load_slots(rowN, ciN, cvN);  // next step's slots in flight during this one
+    const int b = s & 1;
+    if (gl < ELL_W) {
+      s_ci[b][grp][gl] = ci;
+      s_cv[b][grp][gl] = cv;
+    }
+    __syncwarp();
+    const int4 c0 = *reinterpret_cast<const int4*>(&s_ci[b][grp][0]);
+    const int4 c1 = *reinterpret_cast<const int4*>(&s_ci[b][grp][4]);
+    const int cc[ELL_W] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    double g[ELL_W][CPL];
+    unsigned vm = 0;  // slots holding an entry
+#pragma unroll
+    for (int e = 0; e < ELL_W; ++e) {
+      g[e][0] = g[e][1] = 0.0;
+      if (cc[e] >= 0 && any) {
+        double2 q2;
+        gather2(cc[e], row, q2);
+        g[e][0] = q2.x;
+        g[e][1] = q2.y;
+        vm |= 1u << e;
+      }
+    }
+    double a0 = 0.0, a1 = 0.0;
+    const int c7 = cc[ELL_W - 1];
+    const bool longrow = c7 < -1;
+    int st = 0, ln = 0;
+    if (row >= 0 && any) {
+      const double2* vp = reinterpret_cast<const double2*>(&s_cv[b][grp][0]);
+      if (longrow) {  // entry 7 first (the batch runs last-first), from the CSR
+        st = -2 - c7;
+        ln = (int)vp[3].y;
+        const int ce = __ldg(A.indices + st + 7);
+        const double ve = __ldg(A.val + st + 7);
+        const double2 q2 = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)ce * KP));
+        a0 = fma(ve, q2.x, a0);
+        a1 = fma(ve, q2.y, a1);
+      }
+#pragma unroll
+      for (int e2 = ELL_W / 2 - 1; e2 >= 0; --e2) {
+        const double2 vv = vp[e2];
+        if ((vm >> (2 * e2 + 1)) & 1u) {
+          a0 = fma(vv.y, g[2 * e2 + 1][0], a0);
+          a1 = fma(vv.y, g[2 * e2 + 1][1], a1);
+        }
+        if ((vm >> (2 * e2)) & 1u) {
+          a0 = fma(vv.x, g[2 * e2][0], a0);
+          a1 = fma(vv.x, g[2 * e2][1], a1);
+        }
+      }
+    }
+#elif HF_ELL_BCAST
   // Every lane of a row group loads the row's 8 (column, value) slots itself
   // (same-address loads: one L1 wavefront per 16 bytes for the whole row group)
   // instead of receiving them by 16 shuffles: the L1 data pipe, which carries
@@ -912,7 +982,10 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
       if (act1) v[0][1] += pr.y * a1;
     }
     row = rowN;
-#if HF_ELL_BCAST == 1
+#if HF_ELL_SMEM
+    ci = ciN;
+    cv = cvN;
+#elif HF_ELL_BCAST == 1
     c0 = n0;
     c1 = n1;
 #elif HF_ELL_BCAST == 0

@@ -15,17 +15,27 @@ _PATCHES = {
     "fem": ("stiffness_blocks", "volume_stiffness", "assemble_A"),
     "leadfield": ("stiffness_blocks", "pcg_solve", "transfer_matrix", "electrode_response",
                   "eeg_leadfield", "eit_forward", "eit_leadfield"),
-    "cli": ("eeg_leadfield", "eit_leadfield", "eit_forward", "assemble_A", "transfer_matrix"),
-    "experiments": ("eeg_leadfield", "eit_leadfield", "eit_forward", "assemble_A"),
+    "cli": ("eeg_leadfield", "eit_leadfield", "eit_forward", "assemble_A", "transfer_matrix",
+            "generate_mesh"),
+    "experiments": ("eeg_leadfield", "eit_leadfield", "eit_forward", "assemble_A", "generate_mesh"),
+    "meshgen": ("generate_mesh",),
     "simulate": ("eit_forward", "assemble_A", "eeg_leadfield"),
     "": ("ldp", "pcg_solve", "transfer_matrix", "assemble_A", "volume_stiffness",
-         "eeg_leadfield", "eit_forward", "eit_leadfield", "electrode_response"),
+         "eeg_leadfield", "eit_forward", "eit_leadfield", "electrode_response", "generate_mesh"),
 }
 _saved = []
 
 
-def _engine(name):
-    from . import fem, leadfield, solver
+def _engine(name, headfem=None):
+    from . import fem, leadfield, meshgen, solver
+    if name == "generate_mesh":  # returns the caller's own TetMesh type
+        mesh_cls = importlib.import_module(f"{headfem.__name__}.meshgen").TetMesh
+
+        def generate_mesh(seg, h):
+            return meshgen.generate_mesh_device(seg, h).to_mesh(mesh_cls)
+
+        generate_mesh.__doc__ = meshgen.generate_mesh.__doc__
+        return generate_mesh
     for mod in (solver, fem, leadfield):
         if hasattr(mod, name):
             return getattr(mod, name)
@@ -36,6 +46,7 @@ def install(headfem=None):
     """Rebind headfem's lead-field entry points to the B200 engine."""
     if headfem is None:
         headfem = importlib.import_module("headfem")
+    made = {}
     for sub, names in _PATCHES.items():
         try:
             mod = importlib.import_module(f"{headfem.__name__}.{sub}") if sub else headfem
@@ -44,8 +55,21 @@ def install(headfem=None):
         for name in names:
             if hasattr(mod, name):
                 _saved.append((mod, name, getattr(mod, name)))
-                setattr(mod, name, _engine(name))
+                if name not in made:
+                    made[name] = _engine(name, headfem)
+                setattr(mod, name, made[name])
+    # Segmentation.locate is a method (meshgen.py:227,239 and geometry.py:406 call it)
+    geo = importlib.import_module(f"{headfem.__name__}.geometry")
+    _saved.append((geo.Segmentation, "locate", geo.Segmentation.locate))
+    geo.Segmentation.locate = _locate_method
     return headfem
+
+
+def _locate_method(self, points):
+    """Segmentation.locate (geometry.py:359-374) on the device (hf_locate)."""
+    from .meshgen import locate
+
+    return locate(self, points)
 
 
 def uninstall():

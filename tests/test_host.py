@@ -166,11 +166,17 @@ def test_install_rebinds_reference_entry_points():
 
         import paper_1811_07717_b200 as eng
 
-        orig = hs.pcg_solve
+        import headfem.geometry as hg
+        import headfem.meshgen as hm
+
+        orig, orig_gm, orig_loc = hs.pcg_solve, hm.generate_mesh, hg.Segmentation.locate
         eng.install(headfem)
         assert hs.pcg_solve is eng.pcg_solve and hl.transfer_matrix is eng.transfer_matrix
         assert hl.eeg_leadfield is eng.eeg_leadfield
+        assert hm.generate_mesh is not orig_gm and headfem.generate_mesh is hm.generate_mesh
+        assert hg.Segmentation.locate is not orig_loc
         eng.uninstall()
-        assert hs.pcg_solve is orig
+        assert hs.pcg_solve is orig and hm.generate_mesh is orig_gm
+        assert hg.Segmentation.locate is orig_loc
     finally:
         sys.path.remove(ref)
