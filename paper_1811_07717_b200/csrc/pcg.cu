@@ -691,6 +691,9 @@ __global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
 #ifndef HF_ELL_SMEM
 #define HF_ELL_SMEM 1
 #endif
+#ifndef HF_ELL_DIAG0
+#define HF_ELL_DIAG0 0
+#endif
 template <int KP>
 struct Ell {
   static constexpr int CPL = 2;
@@ -705,18 +708,36 @@ __global__ void k_ell_fill(int n, const int32_t* __restrict__ indptr,
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int st = indptr[i], ln = indptr[i + 1] - st;
+  int c[ELL_W];
+  double v[ELL_W];
   for (int e = 0; e < ELL_W; ++e) {
-    int c = -1;
-    double v = 0.0;
+    c[e] = -1;
+    v[e] = 0.0;
     if (ln > ELL_W && e == ELL_W - 1) {
-      c = -2 - st;
-      v = (double)ln;
+      c[e] = -2 - st;
+      v[e] = (double)ln;
     } else if (e < ln) {
-      c = indices[st + e];
-      v = val[st + e];
+      c[e] = indices[st + e];
+      v[e] = val[st + e];
     }
-    eci[(size_t)i * ELL_W + e] = c;
-    ecv[(size_t)i * ELL_W + e] = v;
+  }
+#if HF_ELL_DIAG0
+  // the diagonal (when among the slot-held entries) goes to slot 0, so the
+  // SpMM epilogue takes p_i from its gathered row instead of re-reading it
+  for (int e = 1; e < ELL_W; ++e)
+    if (c[e] == i) {
+      const int tc = c[0];
+      const double tv = v[0];
+      c[0] = c[e];
+      v[0] = v[e];
+      c[e] = tc;
+      v[e] = tv;
+      break;
+    }
+#endif
+  for (int e = 0; e < ELL_W; ++e) {
+    eci[(size_t)i * ELL_W + e] = c[e];
+    ecv[(size_t)i * ELL_W + e] = v[e];
   }
 }
 
@@ -806,6 +827,9 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
     double a0 = 0.0, a1 = 0.0;
     const int c7 = cc[ELL_W - 1];
     const bool longrow = c7 < -1;
+#if HF_ELL_DIAG0
+    const bool dg0 = cc[0] == row;  // slot 0 holds the diagonal: p_i is g[0]
+#endif
     int st = 0, ln = 0;
     if (row >= 0 && any) {
       const double2* vp = reinterpret_cast<const double2*>(&s_cv[b][grp][0]);
@@ -977,7 +1001,12 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
     if (any && row >= 0) {
       const size_t o = (size_t)row * KP + gl * CPL;
       *reinterpret_cast<double2*>(Q + o) = make_double2(a0, a1);
+#if HF_ELL_SMEM && HF_ELL_DIAG0
+      const double2 pr = dg0 ? make_double2(g[0][0], g[0][1])
+                             : __ldg(reinterpret_cast<const double2*>(P + o));
+#else
       const double2 pr = __ldg(reinterpret_cast<const double2*>(P + o));  // L1: the diagonal's gather
+#endif
       if (act0) v[0][0] += pr.x * a0;
       if (act1) v[0][1] += pr.y * a1;
     }
