@@ -694,6 +694,12 @@ __global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
 #ifndef HF_ELL_DIAG0
 #define HF_ELL_DIAG0 0
 #endif
+#ifndef HF_ELL_LEAN
+#define HF_ELL_LEAN 1
+#endif
+#ifndef HF_ELL_LEAN_HB
+#define HF_ELL_LEAN_HB 4
+#endif
 template <int KP>
 struct Ell {
   static constexpr int CPL = 2;
@@ -1022,6 +1028,133 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
     cv = cvN;
 #endif
   }
+  block_partials_map<KP, 1, CPL, LPR>(v, sm, c.part0, nullptr);
+  if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
+  if (tid < KP) {
+    if (s_act[tid]) c.alpha[tid] = c.rz[tid] / tot[tid];
+  }
+}
+
+// ---------------------------------------------------------------- lean ELL SpMM
+// k_spmm_ell2: the same product from a padded ELL copy built so that every
+// slot can be gathered and multiplied unconditionally: empty slots hold
+// (row itself, 0.0), whose gather hits L1 (the row's own p) and whose FMA adds
+// an exact zero.  Rows with more than 8 entries keep entries 0..7 in the slots
+// and flag bit 30 of slot 0's column; their entries 8.. come from the CSR.
+// Sum order: slots 7..0, then entries 8.. in order.  Per row this is ~80
+// instructions instead of ~210 (predicated gathers, zero fills and
+// conditional-FMA selects made the previous kernel issue-bound at 66%).
+constexpr int ELL_LONG = 1 << 30;
+
+__global__ void k_ell_fill2(int n, const int32_t* __restrict__ indptr,
+                            const int32_t* __restrict__ indices, const double* __restrict__ val,
+                            int* __restrict__ eci, double* __restrict__ ecv) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int st = indptr[i], ln = indptr[i + 1] - st;
+  for (int e = 0; e < ELL_W; ++e) {
+    int c = i;
+    double v = 0.0;
+    if (e < ln) {
+      c = indices[st + e];
+      v = val[st + e];
+    }
+    if (e == 0 && ln > ELL_W) c |= ELL_LONG;
+    eci[(size_t)i * ELL_W + e] = c;
+    ecv[(size_t)i * ELL_W + e] = v;
+  }
+}
+
+template <int KP>
+__global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
+    k_spmm_ell2(Ctl c, Csr A, const int* __restrict__ eci, const double* __restrict__ ecv,
+                const double* __restrict__ P, double* __restrict__ Q) {
+  using E = Ell<KP>;
+  constexpr int CPL = E::CPL, LPR = E::LPR, RB = E::RB;
+  __shared__ double sm[NWARP * KP > BLOCK ? NWARP * KP : BLOCK];
+  __shared__ double tot[KP];
+  __shared__ int s_act[KP];
+  __shared__ __align__(16) int s_ci[2][RB][ELL_W];
+  __shared__ __align__(16) double s_cv[2][RB][ELL_W];
+  if (c.summary[SUM_RUN] == 0) return;
+  const int tid = threadIdx.x, gl = tid % LPR, grp = tid / LPR;
+  for (int j = tid; j < KP; j += BLOCK) s_act[j] = (c.state[j] == S_RUN);
+  __syncthreads();
+  const int act0 = s_act[gl * CPL], act1 = s_act[gl * CPL + 1];
+  const bool any = (act0 | act1) != 0;
+  const double m0 = act0 ? 1.0 : 0.0, m1 = act1 ? 1.0 : 0.0;
+  const int nt = (c.n + RB - 1) / RB;
+  const int slot = gl < ELL_W ? gl : ELL_W - 1;
+  const double* __restrict__ Pl = P + gl * CPL;
+  double v0 = 0.0, v1 = 0.0;
+  int t = blockIdx.x;
+  int row = t * RB + grp;
+  row = (t < nt && row < c.n) ? row : -1;
+  int ci = 0;
+  double cv = 0.0;
+  if (row >= 0) {
+    ci = __ldg(eci + (size_t)row * ELL_W + slot);
+    cv = __ldg(ecv + (size_t)row * ELL_W + slot);
+  }
+  int b = 0;
+  for (; t < nt; t += c.G, b ^= 1) {
+    const int tN = t + c.G;
+    int rowN = tN * RB + grp;
+    rowN = (tN < nt && rowN < c.n) ? rowN : -1;
+    int ciN = 0;
+    double cvN = 0.0;
+    if (rowN >= 0) {  // next step's slots in flight during this one
+      ciN = __ldg(eci + (size_t)rowN * ELL_W + slot);
+      cvN = __ldg(ecv + (size_t)rowN * ELL_W + slot);
+    }
+    if (gl < ELL_W) {
+      s_ci[b][grp][gl] = ci;
+      s_cv[b][grp][gl] = cv;
+    }
+    __syncwarp();
+    if (row >= 0 && any) {
+      const int4 c0 = *reinterpret_cast<const int4*>(&s_ci[b][grp][0]);
+      const int4 c1 = *reinterpret_cast<const int4*>(&s_ci[b][grp][4]);
+      const int cc[ELL_W] = {c0.x & (ELL_LONG - 1), c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+      const double2* vp = reinterpret_cast<const double2*>(&s_cv[b][grp][0]);
+      double a0 = 0.0, a1 = 0.0;
+      constexpr int HB = HF_ELL_LEAN_HB;  // gathers in flight per batch (batches run 7.. first)
+#pragma unroll
+      for (int bt = ELL_W / HB - 1; bt >= 0; --bt) {
+        double2 g[HB];
+#pragma unroll
+        for (int k = 0; k < HB; ++k)
+          g[k] = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)(unsigned)cc[bt * HB + k] * KP));
+#pragma unroll
+        for (int k2 = HB / 2 - 1; k2 >= 0; --k2) {
+          const double2 vv = vp[bt * HB / 2 + k2];
+          a0 = fma(vv.y, g[2 * k2 + 1].x, a0);
+          a1 = fma(vv.y, g[2 * k2 + 1].y, a1);
+          a0 = fma(vv.x, g[2 * k2].x, a0);
+          a1 = fma(vv.x, g[2 * k2].y, a1);
+        }
+      }
+      if (c0.x & ELL_LONG) {  // entries 8.. of a long row, in order
+        const int st = __ldg(A.indptr + row), en = __ldg(A.indptr + row + 1);
+        for (int j = st + ELL_W; j < en; ++j) {
+          const int ce = __ldg(A.indices + j);
+          const double ve = __ldg(A.val + j);
+          const double2 q2 = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)ce * KP));
+          a0 = fma(ve, q2.x, a0);
+          a1 = fma(ve, q2.y, a1);
+        }
+      }
+      const size_t o = (size_t)row * KP + gl * CPL;
+      *reinterpret_cast<double2*>(Q + o) = make_double2(a0, a1);
+      const double2 pr = __ldg(reinterpret_cast<const double2*>(P + o));  // L1: the diagonal's gather
+      v0 = fma(pr.x * a0, m0, v0);
+      v1 = fma(pr.y * a1, m1, v1);
+    }
+    row = rowN;
+    ci = ciN;
+    cv = cvN;
+  }
+  double v[1][CPL] = {{v0, v1}};
   block_partials_map<KP, 1, CPL, LPR>(v, sm, c.part0, nullptr);
   if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
   if (tid < KP) {
@@ -2123,12 +2256,17 @@ int setup(const Layout& L, const hf_csr* A, int n, double tol, int max_iter, Ctl
   ce = cs;
   ell = false;
   if constexpr (Ell<KP>::OK) {
-    ell = !fused && !win && ell_enabled();
+    ell = !fused && !win && ell_enabled() && n < (1 << 30);  // lean ELL: bit 30 flags long rows
     if (ell) {  // ELL copy of the SpMM matrix (once per solve)
       const int nt = (n + Ell<KP>::RB - 1) / Ell<KP>::RB;
       ce.G = std::max(1, std::min(sm_count() * HF_ELL_BPS, (nt + HF_ELL_CT - 1) / HF_ELL_CT));
+#if HF_ELL_LEAN
+      k_ell_fill2<<<(n + 255) / 256, 256, 0, stream>>>(n, A->indptr, A->indices, A->val, L.ell_ci,
+                                                       L.ell_cv);
+#else
       k_ell_fill<<<(n + 255) / 256, 256, 0, stream>>>(n, A->indptr, A->indices, A->val, L.ell_ci,
                                                       L.ell_cv);
+#endif
       HF_LAUNCH_CHECK();
       count_launches(1);
     }
@@ -2147,7 +2285,11 @@ inline void launch_round_spmm(const Ctl& cs, const Ctl& ce, const Csr& csr, cons
   }
   if constexpr (Ell<KP>::OK) {
     if (ell) {
+#if HF_ELL_LEAN
+      k_spmm_ell2<KP><<<ce.G, BLOCK, 0, q>>>(ce, csr, L.ell_ci, L.ell_cv, P, L.Q);
+#else
       k_spmm_ell<KP><<<ce.G, BLOCK, 0, q>>>(ce, csr, L.ell_ci, L.ell_cv, P, L.Q);
+#endif
       return;
     }
   }
