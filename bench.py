@@ -142,7 +142,7 @@ def kernel_roofline(engine, A, rounds=24, config="c2"):
         N.C.byref(op.Ac.struct), N.ptr(op.d), N.ptr(Bb), n, kp, rounds, N.ptr(X), ms,
         N.C.byref(fused), N.ptr(ws), ws.numel(), N.stream_handle()))
     nnz = op.Ac.nnz
-    spmm = "k_spmm_ell" if fused.value & 2 else "k_spmm_pq"
+    spmm = ("k_spmm_ell2" if fused.value & 4 else "k_spmm_ell") if fused.value & 2 else "k_spmm_pq"
     if fused.value & 1:
         # k_xs: x/p update (read x, p, r, dd; write x, p) + next SpMM (write q; CSR);
         # the p rows it gathers were just written and are not re-read from DRAM

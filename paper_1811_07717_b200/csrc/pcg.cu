@@ -1045,6 +1045,13 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
 // instructions instead of ~210 (predicated gathers, zero fills and
 // conditional-FMA selects made the previous kernel issue-bound at 66%).
 constexpr int ELL_LONG = 1 << 30;
+#ifndef HF_ELL_LEAN_OPT
+#define HF_ELL_LEAN_OPT 1
+#endif
+#ifndef HF_ELL_OPT_FROM
+#define HF_ELL_OPT_FROM 5
+#endif
+constexpr int ELL_OPT = HF_ELL_OPT_FROM;  // first slot gathered only when it holds an entry
 
 __global__ void k_ell_fill2(int n, const int32_t* __restrict__ indptr,
                             const int32_t* __restrict__ indices, const double* __restrict__ val,
@@ -1052,16 +1059,35 @@ __global__ void k_ell_fill2(int n, const int32_t* __restrict__ indptr,
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int st = indptr[i], ln = indptr[i + 1] - st;
+  int c[ELL_W];
+  double v[ELL_W];
   for (int e = 0; e < ELL_W; ++e) {
-    int c = i;
-    double v = 0.0;
+    // empty slot: (row, 0.0), gathered unconditionally; with HF_ELL_LEAN_OPT the
+    // slots >= ELL_OPT are gathered only when they hold an entry (-1 = empty)
+    c[e] = (HF_ELL_LEAN_OPT && e >= ELL_OPT) ? -1 : i;
+    v[e] = 0.0;
     if (e < ln) {
-      c = indices[st + e];
-      v = val[st + e];
+      c[e] = indices[st + e];
+      v[e] = val[st + e];
     }
-    if (e == 0 && ln > ELL_W) c |= ELL_LONG;
-    eci[(size_t)i * ELL_W + e] = c;
-    ecv[(size_t)i * ELL_W + e] = v;
+  }
+#if HF_ELL_LEAN_OPT
+  // the diagonal (when slot-held) goes to slot 0: the epilogue's p_i is its gather
+  for (int e = 1; e < ELL_W && e < ln; ++e)
+    if (c[e] == i) {
+      const int tc = c[0];
+      const double tv = v[0];
+      c[0] = c[e];
+      v[0] = v[e];
+      c[e] = tc;
+      v[e] = tv;
+      break;
+    }
+#endif
+  if (ln > ELL_W) c[0] |= ELL_LONG;
+  for (int e = 0; e < ELL_W; ++e) {
+    eci[(size_t)i * ELL_W + e] = c[e];
+    ecv[(size_t)i * ELL_W + e] = v[e];
   }
 }
 
@@ -1118,13 +1144,26 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
       const int cc[ELL_W] = {c0.x & (ELL_LONG - 1), c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
       const double2* vp = reinterpret_cast<const double2*>(&s_cv[b][grp][0]);
       double a0 = 0.0, a1 = 0.0;
+#if HF_ELL_LEAN_OPT
+      double2 g0;  // slot 0's gather: p_i when slot 0 is the diagonal
+#endif
       constexpr int HB = HF_ELL_LEAN_HB;  // gathers in flight per batch (batches run 7.. first)
 #pragma unroll
       for (int bt = ELL_W / HB - 1; bt >= 0; --bt) {
         double2 g[HB];
 #pragma unroll
-        for (int k = 0; k < HB; ++k)
-          g[k] = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)(unsigned)cc[bt * HB + k] * KP));
+        for (int k = 0; k < HB; ++k) {
+          const int e = bt * HB + k;
+          if (HF_ELL_LEAN_OPT && e >= ELL_OPT) {  // optional slot: zero when empty
+            g[k] = make_double2(0.0, 0.0);
+            if (cc[e] >= 0) g[k] = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)cc[e] * KP));
+          } else {
+            g[k] = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)(unsigned)cc[e] * KP));
+          }
+        }
+#if HF_ELL_LEAN_OPT
+        if (bt == 0) g0 = g[0];
+#endif
 #pragma unroll
         for (int k2 = HB / 2 - 1; k2 >= 0; --k2) {
           const double2 vv = vp[bt * HB / 2 + k2];
@@ -1146,7 +1185,11 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
       }
       const size_t o = (size_t)row * KP + gl * CPL;
       *reinterpret_cast<double2*>(Q + o) = make_double2(a0, a1);
+#if HF_ELL_LEAN_OPT
+      const double2 pr = cc[0] == row ? g0 : __ldg(reinterpret_cast<const double2*>(P + o));
+#else
       const double2 pr = __ldg(reinterpret_cast<const double2*>(P + o));  // L1: the diagonal's gather
+#endif
       v0 = fma(pr.x * a0, m0, v0);
       v1 = fma(pr.y * a1, m1, v1);
     }
@@ -2547,7 +2590,7 @@ int profile(const hf_csr* A, const double* d, const double* B, int n, int rounds
   bool fused = false, win = false, ell = false;
   Csr csr{A->indptr, A->indices, A->val};
   if (int rc = setup<KP>(L, A, n, 0.0, 1 << 30, c, cs, ce, fused, win, ell, stream)) return rc;
-  *fused_out = (fused ? 1 : 0) | (ell ? 2 : 0) | (c.xd << 8);
+  *fused_out = (fused ? 1 : 0) | (ell ? 2 : 0) | (ell && HF_ELL_LEAN ? 4 : 0) | (c.xd << 8);
   if (c.xd > 1) rounds = (rounds + XD - 1) / XD * XD;  // whole x-deferral cycles
   HF_CUDA(cudaMemsetAsync(L.counter, 0, sizeof(unsigned int) * 4, stream));
   HF_CUDA(cudaMemsetAsync(L.xmask, 0, sizeof(int) * (XD + 1) * KP, stream));
