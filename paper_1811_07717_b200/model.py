@@ -103,7 +103,10 @@ class TetMesh:
         return self._boundary
 
     def boundary_nodes(self):
-        return np.unique(self.boundary_triangles()[0])
+        if getattr(self, "_bnodes", None) is None:  # cached with the boundary faces (meshgen.py:122-134)
+            self._bnodes = np.unique(self.boundary_triangles()[0])
+            self._bnodes.setflags(write=False)
+        return self._bnodes
 
     def with_sigma(self, sigma):
         return TetMesh(self.nodes, self.tetra, self.labels, sigma)
