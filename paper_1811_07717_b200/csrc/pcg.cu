@@ -649,53 +649,18 @@ __global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
 }
 
 // ---------------------------------------------------------------- SpMM over an ELL copy
-// k_spmm_ell: q = A p, p.q, alpha like k_spmm_pq, from an ELL copy of the
-// SpMM matrix (8 slots per row, built once per solve by k_ell_fill).  The row
-// pointers drop out of the dependency chain: a row's gathers wait on one
-// coalesced 8-slot load that is prefetched a step ahead.  Lanes own 2 columns
-// (128-bit gathers) and the kernel is register-light, so 32-48 warps/SM keep the
-// gathers in flight by occupancy instead of by register pipelining (a
-// microbenchmark of this shape on a C2-sized 7-point operator runs at 0.27 ms
-// vs 0.39 ms for the same gathers behind indptr -> indices).
-//   slot e < 8: (column, value), or (-1, 0) padding;  rows with more than 8
-//   entries keep entries 0..6 in slots 0..6 and put a marker (-2 - start, len)
-//   in slot 7; their entries 7.. are read from the CSR.
-// Sums run in spmm_slots' order (each batch of 8 entries last-first, then
-// entries 16.. in order), so q is bitwise that of k_spmm_pq / k_xs.
+// k_spmm_ell2: q = A p, p.q and alpha like k_spmm_pq, from a padded ELL copy of
+// the SpMM matrix (8 slots per row, built once per solve by k_ell_fill2).  The
+// row pointers drop out of the dependency chain: a row's gathers wait on one
+// coalesced slot load prefetched a step ahead.  Lanes own 2 columns (128-bit
+// gathers), so 32 warps/SM keep the gathers in flight by occupancy.  The
+// predicated first version (k_spmm_ell: empty slots skipped per slot, slots
+// distributed by shuffles) and its variants are A/B-timed in DESIGN.md §3.
 #ifndef HF_ELL
 #define HF_ELL 1
 #endif
-#ifndef HF_ELL_HALF
-#define HF_ELL_HALF 0
-#endif
 #ifndef HF_ELL_BPS
 #define HF_ELL_BPS 2
-#endif
-// HF_ELL_CT: tiles per chunk.  1 = tiles dealt round-robin (tile t -> block
-// t % G).  > 1: a block sweeps CT consecutive tiles before the grid moves on,
-// so the rows a gather reaches within the same x-line / y-neighbour line are
-// re-read from L1 instead of L2 (the grid still sweeps the mesh as one band of
-// G*CT tiles, which keeps the z-plane neighbours in L2).
-#ifndef HF_ELL_CT
-#define HF_ELL_CT 1
-#endif
-// HF_ELL_FAR: gathers of rows farther than this from the output row (the
-// z-plane neighbours of a grid-ordered mesh, used once per SM) skip L1
-// allocation so they do not evict the near rows (0: off).
-#ifndef HF_ELL_FAR
-#define HF_ELL_FAR 0
-#endif
-#ifndef HF_ELL_BCAST
-#define HF_ELL_BCAST 0
-#endif
-#ifndef HF_ELL_SMEM
-#define HF_ELL_SMEM 1
-#endif
-#ifndef HF_ELL_DIAG0
-#define HF_ELL_DIAG0 0
-#endif
-#ifndef HF_ELL_LEAN
-#define HF_ELL_LEAN 1
 #endif
 #ifndef HF_ELL_LEAN_HB
 #define HF_ELL_LEAN_HB 4
@@ -708,342 +673,16 @@ struct Ell {
   static constexpr bool OK = (KP >= 16 && KP <= 64);
 };
 
-__global__ void k_ell_fill(int n, const int32_t* __restrict__ indptr,
-                           const int32_t* __restrict__ indices, const double* __restrict__ val,
-                           int* __restrict__ eci, double* __restrict__ ecv) {
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int st = indptr[i], ln = indptr[i + 1] - st;
-  int c[ELL_W];
-  double v[ELL_W];
-  for (int e = 0; e < ELL_W; ++e) {
-    c[e] = -1;
-    v[e] = 0.0;
-    if (ln > ELL_W && e == ELL_W - 1) {
-      c[e] = -2 - st;
-      v[e] = (double)ln;
-    } else if (e < ln) {
-      c[e] = indices[st + e];
-      v[e] = val[st + e];
-    }
-  }
-#if HF_ELL_DIAG0
-  // the diagonal (when among the slot-held entries) goes to slot 0, so the
-  // SpMM epilogue takes p_i from its gathered row instead of re-reading it
-  for (int e = 1; e < ELL_W; ++e)
-    if (c[e] == i) {
-      const int tc = c[0];
-      const double tv = v[0];
-      c[0] = c[e];
-      v[0] = v[e];
-      c[e] = tc;
-      v[e] = tv;
-      break;
-    }
-#endif
-  for (int e = 0; e < ELL_W; ++e) {
-    eci[(size_t)i * ELL_W + e] = c[e];
-    ecv[(size_t)i * ELL_W + e] = v[e];
-  }
-}
-
-template <int KP>
-__global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
-    k_spmm_ell(Ctl c, Csr A, const int* __restrict__ eci, const double* __restrict__ ecv,
-               const double* __restrict__ P, double* __restrict__ Q) {
-  using E = Ell<KP>;
-  constexpr int CPL = E::CPL, LPR = E::LPR, RB = E::RB;
-  __shared__ double sm[NWARP * KP > BLOCK ? NWARP * KP : BLOCK];
-  __shared__ double tot[KP];
-  __shared__ int s_act[KP];
-  if (c.summary[SUM_RUN] == 0) return;
-  const int tid = threadIdx.x, gl = tid % LPR;
-  for (int j = tid; j < KP; j += BLOCK) s_act[j] = (c.state[j] == S_RUN);
-  __syncthreads();
-  const bool act0 = s_act[gl * CPL] != 0, act1 = s_act[gl * CPL + 1] != 0;
-  const bool any = act0 || act1;
-  const int nt = (c.n + RB - 1) / RB;
-  const int slot = gl < ELL_W ? gl : ELL_W - 1;  // lane gl holds slot gl (lanes >= 8: unused copy)
-  auto row_at = [&](int t) {
-    const int r = t * RB + tid / LPR;
-    return (t < nt && r < c.n) ? r : -1;
-  };
-  auto load_slots = [&](int r, int& ci, double& cv) {
-    ci = -1;
-    cv = 0.0;
-    if (r >= 0) {
-      ci = __ldg(eci + (size_t)r * ELL_W + slot);
-      cv = __ldg(ecv + (size_t)r * ELL_W + slot);
-    }
-  };
-  const double* __restrict__ Pl = P + gl * CPL;
-  double v[1][CPL] = {{0.0, 0.0}};
-  // slot s of this block -> tile (chunks of HF_ELL_CT consecutive tiles, dealt round-robin)
-  auto tile_of = [&](int s) {
-    if constexpr (HF_ELL_CT == 1) return (int)blockIdx.x + s * c.G;
-    else return ((s / HF_ELL_CT) * c.G + (int)blockIdx.x) * HF_ELL_CT + s % HF_ELL_CT;
-  };
-  auto gather2 = [&](int cc, int r, double2& q2) {
-    const double* gp = Pl + (size_t)cc * KP;
-    if (HF_ELL_FAR > 0 && abs(cc - r) > HF_ELL_FAR) {
-      asm("ld.global.nc.L1::no_allocate.v2.f64 {%0,%1}, [%2];" : "=d"(q2.x), "=d"(q2.y) : "l"(gp));
-    } else {
-      q2 = __ldg(reinterpret_cast<const double2*>(gp));
-    }
-  };
-#if HF_ELL_SMEM
-  // The row's 8 (column, value) slots reach every lane of its row group through
-  // a per-group shared-memory slot (lanes 0..7 store them, then LDS.128
-  // broadcasts) instead of 26 SHFL.32 (a double shuffles as two): the L1 data
-  // pipe carries both and is this kernel's busiest unit (82% at C2), and the
-  // broadcast reads cost 6 wavefronts per row instead of 26.  Slots of the next
-  // row stay prefetched in registers (lanes 0..7), buffers alternate by step.
-  __shared__ __align__(16) int s_ci[2][RB][ELL_W];
-  __shared__ __align__(16) double s_cv[2][RB][ELL_W];
-  const int grp = tid / LPR;
-  int s = 0, t = tile_of(0);
-  int row = row_at(t), ci, ciN;
-  double cv, cvN;
-  load_slots(row, ci, cv);
-  for (; t < nt; t = tile_of(++s)) {
-    const int rowN = row_at(tile_of(s + 1));
-    load_slots(rowN, ciN, cvN);  // next step's slots in flight during this one
-    const int b = s & 1;
-    if (gl < ELL_W) {
-      s_ci[b][grp][gl] = ci;
-      s_cv[b][grp][gl] = cv;
-    }
-    __syncwarp();
-    const int4 c0 = *reinterpret_cast<const int4*>(&s_ci[b][grp][0]);
-    const int4 c1 = *reinterpret_cast<const int4*>(&s_ci[b][grp][4]);
-    const int cc[ELL_W] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-    double g[ELL_W][CPL];
-    unsigned vm = 0;  // slots holding an entry
-#pragma unroll
-    for (int e = 0; e < ELL_W; ++e) {
-      g[e][0] = g[e][1] = 0.0;
-      if (cc[e] >= 0 && any) {
-        double2 q2;
-        gather2(cc[e], row, q2);
-        g[e][0] = q2.x;
-        g[e][1] = q2.y;
-        vm |= 1u << e;
-      }
-    }
-    double a0 = 0.0, a1 = 0.0;
-    const int c7 = cc[ELL_W - 1];
-    const bool longrow = c7 < -1;
-#if HF_ELL_DIAG0
-    const bool dg0 = cc[0] == row;  // slot 0 holds the diagonal: p_i is g[0]
-#endif
-    int st = 0, ln = 0;
-    if (row >= 0 && any) {
-      const double2* vp = reinterpret_cast<const double2*>(&s_cv[b][grp][0]);
-      if (longrow) {  // entry 7 first (the batch runs last-first), from the CSR
-        st = -2 - c7;
-        ln = (int)vp[3].y;
-        const int ce = __ldg(A.indices + st + 7);
-        const double ve = __ldg(A.val + st + 7);
-        const double2 q2 = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)ce * KP));
-        a0 = fma(ve, q2.x, a0);
-        a1 = fma(ve, q2.y, a1);
-      }
-#pragma unroll
-      for (int e2 = ELL_W / 2 - 1; e2 >= 0; --e2) {
-        const double2 vv = vp[e2];
-        if ((vm >> (2 * e2 + 1)) & 1u) {
-          a0 = fma(vv.y, g[2 * e2 + 1][0], a0);
-          a1 = fma(vv.y, g[2 * e2 + 1][1], a1);
-        }
-        if ((vm >> (2 * e2)) & 1u) {
-          a0 = fma(vv.x, g[2 * e2][0], a0);
-          a1 = fma(vv.x, g[2 * e2][1], a1);
-        }
-      }
-    }
-#elif HF_ELL_BCAST
-  // Every lane of a row group loads the row's 8 (column, value) slots itself
-  // (same-address loads: one L1 wavefront per 16 bytes for the whole row group)
-  // instead of receiving them by 16 shuffles: the L1 data pipe, which carries
-  // both, is this kernel's busiest unit (82% at C2).  Values are loaded after the
-  // gathers are issued, so their latency hides under the gathers'.
-  auto load_ci = [&](int r, int4& x0, int4& x1) {
-    if (r >= 0) {
-      x0 = __ldg(reinterpret_cast<const int4*>(eci + (size_t)r * ELL_W));
-      x1 = __ldg(reinterpret_cast<const int4*>(eci + (size_t)r * ELL_W) + 1);
-    } else {
-      x0 = x1 = make_int4(-1, -1, -1, -1);
-    }
-  };
-  int s = 0, t = tile_of(0);
-  int row = row_at(t);
-#if HF_ELL_BCAST == 2
-  for (; t < nt; t = tile_of(++s)) {  // slots of the next row prefetched into L1, not registers
-    const int rowN = row_at(tile_of(s + 1));
-    if (rowN >= 0 && gl == 0) {
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(eci + (size_t)rowN * ELL_W));
-      asm volatile("prefetch.global.L1 [%0];" ::"l"(ecv + (size_t)rowN * ELL_W));
-    }
-    int4 c0, c1;
-    load_ci(row, c0, c1);
-#else
-  int4 c0, c1;
-  load_ci(row, c0, c1);
-  for (; t < nt; t = tile_of(++s)) {
-    const int rowN = row_at(tile_of(s + 1));
-    int4 n0, n1;
-    load_ci(rowN, n0, n1);  // next step's columns in flight during this one
-#endif
-    const int cc[ELL_W] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-    double g[ELL_W][CPL];
-#pragma unroll
-    for (int e = 0; e < ELL_W; ++e) {
-      g[e][0] = g[e][1] = 0.0;
-      if (cc[e] >= 0 && any) {
-        double2 q2;
-        gather2(cc[e], row, q2);
-        g[e][0] = q2.x;
-        g[e][1] = q2.y;
-      }
-    }
-    double a0 = 0.0, a1 = 0.0;
-    const bool longrow = cc[ELL_W - 1] < -1;
-    int st = 0, ln = 0;
-    if (row >= 0 && any) {
-      const double2* vp = reinterpret_cast<const double2*>(ecv + (size_t)row * ELL_W);
-      const double2 v01 = __ldg(vp), v23 = __ldg(vp + 1), v45 = __ldg(vp + 2), v67 = __ldg(vp + 3);
-      const double vv[ELL_W] = {v01.x, v01.y, v23.x, v23.y, v45.x, v45.y, v67.x, v67.y};
-      if (longrow) {  // entry 7 first (the batch runs last-first), from the CSR
-        st = -2 - cc[ELL_W - 1];
-        ln = (int)vv[ELL_W - 1];
-        const int ce = __ldg(A.indices + st + 7);
-        const double ve = __ldg(A.val + st + 7);
-        const double2 q2 = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)ce * KP));
-        a0 = fma(ve, q2.x, a0);
-        a1 = fma(ve, q2.y, a1);
-      }
-#pragma unroll
-      for (int e = ELL_W - 1; e >= 0; --e) {
-        if (cc[e] >= 0) {
-          a0 = fma(vv[e], g[e][0], a0);
-          a1 = fma(vv[e], g[e][1], a1);
-        }
-      }
-    }
-#else
-  int s = 0, t = tile_of(0);
-  int row = row_at(t), ci, ciN;
-  double cv, cvN;
-  load_slots(row, ci, cv);
-  for (; t < nt; t = tile_of(++s)) {
-    const int rowN = row_at(tile_of(s + 1));
-    load_slots(rowN, ciN, cvN);  // next step's slots in flight during this one
-    // slots in batches of HB gathers, consumed last-first (slot 7 .. slot 0)
-    constexpr int HB = HF_ELL_HALF ? 4 : ELL_W, NBT = ELL_W / HB;
-    unsigned vm = 0;  // slots holding an entry
-    int c7 = -1, st = 0, ln = 0;
-    bool longrow = false;
-    double a0 = 0.0, a1 = 0.0;
-    const double cv7 = __shfl_sync(FULL, cv, ELL_W - 1, LPR);  // (outside divergent branches)
-#pragma unroll
-    for (int bt = NBT - 1; bt >= 0; --bt) {
-      double g[HB][CPL];
-#pragma unroll
-      for (int k = 0; k < HB; ++k) {
-        const int e = bt * HB + k;
-        const int cc = __shfl_sync(FULL, ci, e, LPR);
-        g[k][0] = g[k][1] = 0.0;
-        if (cc >= 0 && any) {
-          double2 q2;
-          gather2(cc, row, q2);
-          g[k][0] = q2.x;
-          g[k][1] = q2.y;
-        }
-        vm |= (cc >= 0 && any) ? 1u << e : 0u;
-        if (e == ELL_W - 1) c7 = cc;
-      }
-      if (bt == NBT - 1) {
-        longrow = c7 < -1;
-        if (longrow) {  // entry 7 first (batch 0 runs last-first), from the CSR
-          st = -2 - c7;
-          ln = (int)cv7;
-          if (any) {
-            const int ce = __ldg(A.indices + st + 7);
-            const double ve = __ldg(A.val + st + 7);
-            const double2 q2 = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)ce * KP));
-            a0 = fma(ve, q2.x, a0);
-            a1 = fma(ve, q2.y, a1);
-          }
-        }
-      }
-#pragma unroll
-      for (int k = HB - 1; k >= 0; --k) {
-        const int e = bt * HB + k;
-        const double vv = __shfl_sync(FULL, cv, e, LPR);
-        if ((vm >> e) & 1u) {
-          a0 = fma(vv, g[k][0], a0);
-          a1 = fma(vv, g[k][1], a1);
-        }
-      }
-    }
-#endif
-    if (longrow && any) {  // entries 8..15 last-first, then 16.. in order
-      const int hi = min(ln, 16);
-      for (int e = hi - 1; e >= 8; --e) {
-        const int ce = __ldg(A.indices + st + e);
-        const double ve = __ldg(A.val + st + e);
-        const double2 q2 = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)ce * KP));
-        a0 = fma(ve, q2.x, a0);
-        a1 = fma(ve, q2.y, a1);
-      }
-      for (int e = 16; e < ln; ++e) {
-        const int ce = __ldg(A.indices + st + e);
-        const double ve = __ldg(A.val + st + e);
-        const double2 q2 = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)ce * KP));
-        a0 = fma(ve, q2.x, a0);
-        a1 = fma(ve, q2.y, a1);
-      }
-    }
-    if (any && row >= 0) {
-      const size_t o = (size_t)row * KP + gl * CPL;
-      *reinterpret_cast<double2*>(Q + o) = make_double2(a0, a1);
-#if HF_ELL_SMEM && HF_ELL_DIAG0
-      const double2 pr = dg0 ? make_double2(g[0][0], g[0][1])
-                             : __ldg(reinterpret_cast<const double2*>(P + o));
-#else
-      const double2 pr = __ldg(reinterpret_cast<const double2*>(P + o));  // L1: the diagonal's gather
-#endif
-      if (act0) v[0][0] += pr.x * a0;
-      if (act1) v[0][1] += pr.y * a1;
-    }
-    row = rowN;
-#if HF_ELL_SMEM
-    ci = ciN;
-    cv = cvN;
-#elif HF_ELL_BCAST == 1
-    c0 = n0;
-    c1 = n1;
-#elif HF_ELL_BCAST == 0
-    ci = ciN;
-    cv = cvN;
-#endif
-  }
-  block_partials_map<KP, 1, CPL, LPR>(v, sm, c.part0, nullptr);
-  if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
-  if (tid < KP) {
-    if (s_act[tid]) c.alpha[tid] = c.rz[tid] / tot[tid];
-  }
-}
-
-// ---------------------------------------------------------------- lean ELL SpMM
-// k_spmm_ell2: the same product from a padded ELL copy built so that every
-// slot can be gathered and multiplied unconditionally: empty slots hold
-// (row itself, 0.0), whose gather hits L1 (the row's own p) and whose FMA adds
-// an exact zero.  Rows with more than 8 entries keep entries 0..7 in the slots
-// and flag bit 30 of slot 0's column; their entries 8.. come from the CSR.
-// Sum order: slots 7..0, then entries 8.. in order.  Per row this is ~80
-// instructions instead of ~210 (predicated gathers, zero fills and
-// conditional-FMA selects made the previous kernel issue-bound at 66%).
+// The ELL copy is built so that slots can be gathered and multiplied
+// unconditionally: empty slots 0..ELL_OPT-1 hold (row itself, 0.0), whose
+// gather hits L1 (the row's own p) and whose FMA adds an exact zero; empty
+// slots from ELL_OPT on hold -1 and are skipped (an interior row fills 7).  The
+// diagonal sits in slot 0, so the epilogue's p_i is its gather.  Rows with more
+// than 8 entries keep entries 0..7 in the slots and flag bit 30 of slot 0's
+// column; their entries 8.. come from the CSR.  Sum order: slots 7..0, then
+// entries 8.. in order.  ~110 instructions per row instead of ~210 (predicated
+// gathers, zero fills and conditional-FMA selects made the predicated kernel
+// issue-bound at 66%).
 constexpr int ELL_LONG = 1 << 30;
 #ifndef HF_ELL_LEAN_OPT
 #define HF_ELL_LEAN_OPT 1
@@ -2155,7 +1794,7 @@ struct Layout {
   int4* tinfo;       // k_spmm_win tile windows
   int2* tranges;
   uint16_t* eslot;
-  int* ell_ci;     // k_spmm_ell: 8 slots per row (see k_ell_fill)
+  int* ell_ci;     // k_spmm_ell2: 8 slots per row (see k_ell_fill2)
   double* ell_cv;
   size_t bytes;
 };
@@ -2215,7 +1854,7 @@ __global__ void k_bandwidth(int n, const int32_t* __restrict__ indptr,
 // 128-register budget, its streaming half runs at 16 warps/SM and loses to
 // the three-kernel round (1.28 vs 1.00 ms at C2, kp=64).  Opt in with
 // HFB200_FUSED=1 while it is being reworked (warp-specialised x/p warps).
-// k_spmm_ell for kp 16..64 (default); HFB200_ELL=0 selects the CSR kernel k_spmm_pq.
+// k_spmm_ell2 for kp 16..64 (default); HFB200_ELL=0 selects the CSR kernel k_spmm_pq.
 inline bool ell_enabled() {
   const char* v = getenv("HFB200_ELL");
   return HF_ELL && !(v && v[0] == '0');
@@ -2302,14 +1941,9 @@ int setup(const Layout& L, const hf_csr* A, int n, double tol, int max_iter, Ctl
     ell = !fused && !win && ell_enabled() && n < (1 << 30);  // lean ELL: bit 30 flags long rows
     if (ell) {  // ELL copy of the SpMM matrix (once per solve)
       const int nt = (n + Ell<KP>::RB - 1) / Ell<KP>::RB;
-      ce.G = std::max(1, std::min(sm_count() * HF_ELL_BPS, (nt + HF_ELL_CT - 1) / HF_ELL_CT));
-#if HF_ELL_LEAN
+      ce.G = std::max(1, std::min(sm_count() * HF_ELL_BPS, nt));
       k_ell_fill2<<<(n + 255) / 256, 256, 0, stream>>>(n, A->indptr, A->indices, A->val, L.ell_ci,
                                                        L.ell_cv);
-#else
-      k_ell_fill<<<(n + 255) / 256, 256, 0, stream>>>(n, A->indptr, A->indices, A->val, L.ell_ci,
-                                                      L.ell_cv);
-#endif
       HF_LAUNCH_CHECK();
       count_launches(1);
     }
@@ -2328,11 +1962,7 @@ inline void launch_round_spmm(const Ctl& cs, const Ctl& ce, const Csr& csr, cons
   }
   if constexpr (Ell<KP>::OK) {
     if (ell) {
-#if HF_ELL_LEAN
       k_spmm_ell2<KP><<<ce.G, BLOCK, 0, q>>>(ce, csr, L.ell_ci, L.ell_cv, P, L.Q);
-#else
-      k_spmm_ell<KP><<<ce.G, BLOCK, 0, q>>>(ce, csr, L.ell_ci, L.ell_cv, P, L.Q);
-#endif
       return;
     }
   }
@@ -2590,7 +2220,7 @@ int profile(const hf_csr* A, const double* d, const double* B, int n, int rounds
   bool fused = false, win = false, ell = false;
   Csr csr{A->indptr, A->indices, A->val};
   if (int rc = setup<KP>(L, A, n, 0.0, 1 << 30, c, cs, ce, fused, win, ell, stream)) return rc;
-  *fused_out = (fused ? 1 : 0) | (ell ? 2 : 0) | (ell && HF_ELL_LEAN ? 4 : 0) | (c.xd << 8);
+  *fused_out = (fused ? 1 : 0) | (ell ? 6 : 0) | (c.xd << 8);  // 4: the lean ELL kernel
   if (c.xd > 1) rounds = (rounds + XD - 1) / XD * XD;  // whole x-deferral cycles
   HF_CUDA(cudaMemsetAsync(L.counter, 0, sizeof(unsigned int) * 4, stream));
   HF_CUDA(cudaMemsetAsync(L.xmask, 0, sizeof(int) * (XD + 1) * KP, stream));

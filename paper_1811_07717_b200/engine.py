@@ -23,7 +23,7 @@ import scipy.sparse as sp
 import torch
 
 from . import model
-from .device import DeviceCsr, PcgOperator, device
+from .device import DeviceCsr, PcgOperator, device, to_device
 from .fem import DeviceMesh, assemble_device, blocks_device
 from .leadfield import lf_tail_device, response_block_device, response_operator, symmetrize
 from .solver import PcgConfig, _raise_failed, rhs_block, solve_block
@@ -52,9 +52,8 @@ class EegEngine:
         self.h2d_bytes = 0
         self.dmesh = DeviceMesh(mesh.nodes, mesh.tetra, dev)
         self.h2d_bytes += self.dmesh.nodes.numel() * 8 + self.dmesh.tetra.numel() * 4
-        sig = np.array(mesh.sigma, dtype=np.float64, order="C")
-        self.sigma = torch.from_numpy(sig).to(dev)
-        self.h2d_bytes += sig.nbytes
+        self.sigma = to_device(mesh.sigma, np.float64, dev, slot=2)
+        self.h2d_bytes += self.sigma.numel() * 8
         if B is None or C is None or R is None:
             B, C, R = model.assemble_B_C_R(mesh, electrodes)
         self.L = B.shape[1]

@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .device import DeviceCsr, device
+from .device import DeviceCsr, device, to_device
 from .errors import AssemblyError
 from .model import ground_node, electrode_contacts
 
@@ -38,8 +38,8 @@ class DeviceMesh:
         dev = dev or device()
         self.n = int(len(nodes))
         self.m = int(len(tetra))
-        self.nodes = torch.from_numpy(np.array(nodes, dtype=np.float64, order="C")).to(dev)
-        self.tetra = torch.from_numpy(np.array(tetra, dtype=np.int32, order="C")).to(dev)
+        self.nodes = to_device(nodes, np.float64, dev, slot=0)
+        self.tetra = to_device(tetra, np.int32, dev, slot=1)
 
     @classmethod
     def of(cls, mesh):
