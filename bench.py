@@ -130,7 +130,7 @@ def kernel_roofline(engine, A, rounds=24, config="c2"):
 
     op = PcgOperator(A, "ldp")
     n = op.n
-    kp = width_for(min(MAX_BATCH, engine.Bd.shape[1]))
+    kp = width_for(op.batch_width(engine.Bd.shape[1], MAX_BATCH))  # the solver's own batch width
     Bb = torch.zeros((n, kp), dtype=torch.float64, device=engine.Bd.device)
     k = min(kp, engine.Bd.shape[1])
     Bb[:, :k] = engine.Bd[:, :k]

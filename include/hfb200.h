@@ -14,6 +14,7 @@
  * `headfem` (files relative to /root/reference/pkg/src/headfem/):
  *
  *   hf_ldp                 solver.py:50-61     ldp(A)
+ *   hf_csr_bandwidth       (internal)          gather reach of A, sizes the PCG batch width
  *   hf_pcg_multi           solver.py:64-111    pcg_solve(A, b, cfg), one column per RHS
  *                          solver.py:114-141   transfer_matrix(A, B, cfg, threads)
  *   hf_pcg_profile         (bench)             per-kernel CUDA-event timing of a PCG round
@@ -92,6 +93,12 @@ int hf_exclusive_scan_i32(const int32_t* in, int32_t* out, int32_t n, int32_t* t
  * scratch; *n_zero_rows (host) receives the number of rows with d_i == 0 (the
  * caller raises SingularPreconditionerError).  Synchronises `stream`. */
 int hf_ldp(const hf_csr* A, double* d, int32_t* zero_count, int32_t* n_zero_rows, void* stream);
+
+/* Matrix bandwidth max_i max(i - first col, last col - i) of a CSR with sorted
+ * rows (the reach of the SpMM's gathers; the solver sizes its batch width so
+ * the rows one sweep touches twice stay in L2).  scratch: one device int32;
+ * *bandwidth (host).  Synchronises `stream`. */
+int hf_csr_bandwidth(const hf_csr* A, int32_t* scratch, int32_t* bandwidth, void* stream);
 
 /* Zero-free copy of A used by the SpMM (explicit zeros add 0*x, an exact
  * no-op for finite x).  Two steps: count (returns nnz of the copy on host),

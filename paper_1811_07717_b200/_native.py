@@ -45,6 +45,7 @@ def _load():
         "hf_scan_workspace_bytes": (SZ, [I32]),
         "hf_exclusive_scan_i32": (C.c_int, [P, P, I32, P, P, SZ, P]),
         "hf_ldp": (C.c_int, [pcsr, P, P, C.POINTER(I32), P]),
+        "hf_csr_bandwidth": (C.c_int, [pcsr, P, C.POINTER(I32), P]),
         "hf_csr_prune_workspace_bytes": (SZ, [I32]),
         "hf_csr_prune_count": (C.c_int, [pcsr, P, SZ, C.POINTER(I64), P]),
         "hf_csr_prune_fill": (C.c_int, [pcsr, P, SZ, P, P, P, P]),
@@ -81,7 +82,7 @@ lib = _load()
 
 # Every symbol include/hfb200.h declares (checked by tests/test_abi.py).
 EXPORTED = ("hf_version", "hf_last_error", "hf_device_sm_count", "hf_launch_count", "hf_scan_workspace_bytes",
-            "hf_exclusive_scan_i32", "hf_ldp",
+            "hf_exclusive_scan_i32", "hf_ldp", "hf_csr_bandwidth",
             "hf_csr_prune_workspace_bytes", "hf_csr_prune_count", "hf_csr_prune_fill",
             "hf_pcg_workspace_bytes", "hf_pcg_multi", "hf_pcg_profile", "hf_p1_blocks",
             "hf_p1_assemble_workspace_bytes", "hf_p1_assemble_prepare", "hf_p1_assemble_fill",

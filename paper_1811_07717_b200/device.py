@@ -139,6 +139,9 @@ def ldp_device(A: DeviceCsr):
     return d, int(nz.value)
 
 
+L2_WINDOW = 48 << 20  # bytes of the 126 MB L2 the SpMM's two-plane reuse window may take
+
+
 class PcgOperator:
     """A prepared for the multi-RHS solver: parity CSR, zero-free SpMM copy and
     the preconditioner diagonal (computed once, not once per column as
@@ -155,6 +158,23 @@ class PcgOperator:
             self.d = torch.ones(self.n, dtype=torch.float64, device=A.val.device)
             self.n_zero_rows = 0
         self.Ac = A.pruned()
+        scratch = torch.empty(1, dtype=torch.int32, device=A.val.device)
+        bw = N.C.c_int32(0)
+        N.check("hf_csr_bandwidth", N.lib.hf_csr_bandwidth(N.C.byref(self.Ac.struct), N.ptr(scratch),
+                                                           N.C.byref(bw), N.stream_handle()))
+        self.bandwidth = int(bw.value)
+
+    def batch_width(self, k, cap):
+        """RHS columns per multi-RHS solve: `cap`, halved (not below 16) while the
+        p and q rows one sweep reaches twice (about 2 x bandwidth rows each, kp
+        doubles per row) would fill more than L2_WINDOW bytes of the 126 MB L2.
+        C2 (bandwidth ~15k rows) keeps 64; the 5M-node C5 mesh (~35k) runs at 32,
+        3% faster per column than 64 (its q/p window at 64 is 72 MB and its
+        SpMM re-reads p from DRAM)."""
+        w = cap
+        while w > 16 and 4 * self.bandwidth * w * 8 > L2_WINDOW:
+            w //= 2
+        return min(w, k) if k > 0 else w
 
 
 def width_for(k):

@@ -117,6 +117,7 @@ def solve_block(op, B, cfg=PcgConfig(), batch=MAX_BATCH, out=None):
     X = out if out is not None else torch.empty((n, k), dtype=torch.float64, device=B.device)
     info = SolveInfo(np.zeros(k, np.int64), np.zeros(k, np.int64), np.zeros(k), np.ones(k),
                      np.zeros(k, np.int64), max_iter)
+    batch = max(1, op.batch_width(k, batch))
     for c0 in range(0, k, batch):
         c1 = min(k, c0 + batch)
         kb = c1 - c0
