@@ -100,17 +100,6 @@ struct Csr {
   const double* __restrict__ val;
 };
 
-// Programmatic dependent launch (PDL).  The round kernels are launched with
-// programmatic stream serialisation (launch_k): a kernel's CTAs may be placed
-// on SMs as soon as the previous kernel's CTAs exit, and wait here until that
-// grid has completed and its memory is visible.  This hides the launch gap and
-// the CTA ramp behind the previous kernel's tail (its last-block reduction).
-// Both are no-ops for an ordinary launch.
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() {
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-}
-
 template <int KP>
 struct Map {
   static constexpr int CPL = (KP >= 64) ? 4 : 2;  // columns per lane: one 256/128-bit access
@@ -745,8 +734,6 @@ template <int KP>
 __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
     k_spmm_ell2(Ctl c, Csr A, const int* __restrict__ eci, const double* __restrict__ ecv,
                 const double* __restrict__ P, double* __restrict__ Q) {
-  pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
-  pdl_trigger();
   using E = Ell<KP>;
   constexpr int CPL = E::CPL, LPR = E::LPR, RB = E::RB;
   __shared__ double sm[NWARP * KP > BLOCK ? NWARP * KP : BLOCK];
@@ -861,8 +848,6 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
 template <int KP>
 __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
     k_update_r(Ctl c, const double* __restrict__ Q, double* R) {
-  pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
-  pdl_trigger();
   using M = Map<KP>;
   __shared__ double sm[2 * M::RED];
   __shared__ double tot[2 * KP];
@@ -1052,8 +1037,6 @@ template <int KP>
 __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
     k_update_p(Ctl c, const double* __restrict__ Pcur, double* __restrict__ Pnext,
                const double* __restrict__ R) {
-  pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
-  pdl_trigger();
   using M = Map<KP>;
   __shared__ double s_beta[KP];
   __shared__ int s_pm[KP];
@@ -1110,8 +1093,6 @@ __global__ void __launch_bounds__(BLOCK, 1)
     k_update_xring(Ctl c, double* __restrict__ X, double* __restrict__ Pring, size_t nk,
                    const double* __restrict__ R, const double* __restrict__ alpha_h,
                    const int* __restrict__ xmask_h) {
-  pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
-  pdl_trigger();
   using M = Map<KP>;
   __shared__ double s_alpha[XD][KP];
   __shared__ int s_xm[XD][KP];
@@ -1184,8 +1165,6 @@ __global__ void __launch_bounds__(BLOCK, 1)
 template <int KP>
 __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
     k_replace_p(Ctl c, double* __restrict__ Pring, size_t nk, const double* __restrict__ R) {
-  pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
-  pdl_trigger();
   using M = Map<KP>;
   __shared__ int s_pm[KP], s_buf[KP];
   __shared__ double s_beta[KP];
@@ -1671,8 +1650,6 @@ template <int KP>
 __global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
     k_spmm_resid(Ctl c, Csr A, const double* __restrict__ B, const double* __restrict__ X,
                  double* __restrict__ Q) {
-  pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
-  pdl_trigger();
   using M = Map<KP>;
   __shared__ double sm[M::RED];
   __shared__ double tot[KP];
@@ -1737,8 +1714,6 @@ __global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
 template <int KP>
 __global__ void __launch_bounds__(BLOCK, BLOCKS_PER_SM)
     k_replace(Ctl c, const double* __restrict__ Q, double* R) {
-  pdl_wait();  // programmatic dependent launch: the previous kernel's writes are visible
-  pdl_trigger();
   using M = Map<KP>;
   __shared__ double sm[M::RED];
   __shared__ double tot[KP];
@@ -1976,40 +1951,6 @@ int setup(const Layout& L, const hf_csr* A, int n, double tol, int max_iter, Ctl
   return HF_OK;
 }
 
-// Round kernels go through launch_k: with PDL on (default; HFB200_PDL=0 turns
-// it off) each is launched with programmatic stream serialisation, which
-// stream capture records as a programmatic edge of the chunk graph.
-static thread_local cudaError_t t_launch_err = cudaSuccess;
-
-inline bool pdl_enabled() {
-  static const bool on = [] {
-    const char* v = getenv("HFB200_PDL");
-    return !(v && v[0] == '0');
-  }();
-  return on;
-}
-
-template <typename... KArgs, typename... Args>
-inline void launch_k(void (*kern)(KArgs...), int grid, cudaStream_t q, Args... args) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(BLOCK);
-  cfg.stream = q;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
-  if (e != cudaSuccess) t_launch_err = e;  // surfaced by the caller (take_launch_error)
-}
-
-inline cudaError_t take_launch_error() {
-  const cudaError_t e = t_launch_err;
-  t_launch_err = cudaSuccess;
-  return e;
-}
-
 // The unfused round's SpMM: the TMA-window, ELL or CSR kernel.
 template <int KP>
 inline void launch_round_spmm(const Ctl& cs, const Ctl& ce, const Csr& csr, const Layout& L,
@@ -2021,7 +1962,7 @@ inline void launch_round_spmm(const Ctl& cs, const Ctl& ce, const Csr& csr, cons
   }
   if constexpr (Ell<KP>::OK) {
     if (ell) {
-      launch_k(k_spmm_ell2<KP>, ce.G, q, ce, csr, (const int*)L.ell_ci, (const double*)L.ell_cv, P, L.Q);
+      k_spmm_ell2<KP><<<ce.G, BLOCK, 0, q>>>(ce, csr, L.ell_ci, L.ell_cv, P, L.Q);
       return;
     }
   }
@@ -2055,17 +1996,15 @@ inline void launch_round_timed(const Ctl& c0, const Ctl& cs0, const Ctl& ce0, co
   double* Pc = L.P + (size_t)slot * nk;
   launch_round_spmm<KP>(cs, ce, csr, L, Pc, win, ell, q);
   if (ev) cudaEventRecord(ev[1], q);
-  launch_k(k_update_r<KP>, c.G, q, c, (const double*)L.Q, L.R);
+  k_update_r<KP><<<c.G, BLOCK, 0, q>>>(c, L.Q, L.R);
   if (ev) cudaEventRecord(ev[2], q);
   if (slot == XD - 1) {
     const int gx = std::max(1, std::min(sm_count(), n_tiles(c.n, Map<KP>::RB)));
     Ctl cx = c;
     cx.G = gx;
-    launch_k(k_update_xring<KP>, gx, q, cx, X, L.P, nk, (const double*)L.R, (const double*)L.alpha,
-             (const int*)L.xmask);
+    k_update_xring<KP><<<gx, BLOCK, 0, q>>>(cx, X, L.P, nk, L.R, L.alpha, L.xmask);
   } else {
-    launch_k(k_update_p<KP>, c.G, q, c, (const double*)Pc, L.P + (size_t)(slot + 1) * nk,
-             (const double*)L.R);
+    k_update_p<KP><<<c.G, BLOCK, 0, q>>>(c, Pc, L.P + (size_t)(slot + 1) * nk, L.R);
   }
   if (ev) cudaEventRecord(ev[3], q);
 }
@@ -2081,15 +2020,15 @@ template <int KP>
 inline void launch_check(const Ctl& c0, const Ctl& cs, const Csr& csr, const Layout& L,
                          const double* B, double* X, cudaStream_t q) {
   Ctl c = c0;
-  launch_k(k_spmm_resid<KP>, cs.G, q, cs, csr, B, (const double*)X, L.Q);
+  k_spmm_resid<KP><<<cs.G, BLOCK, 0, q>>>(cs, csr, B, X, L.Q);
   if (c.xd == 1) {
     k_replace<KP><<<c.G, BLOCK, 0, q>>>(c, L.Q, L.R);
     k_update_xp<KP><<<c.G, BLOCK, 0, q>>>(c, SUM_REPLACE, X, L.P, L.R);
     return;
   }
   c.xmask = L.xmask + (size_t)XD * KP;  // scratch: the round slots stay untouched
-  launch_k(k_replace<KP>, c.G, q, c, (const double*)L.Q, L.R);
-  launch_k(k_replace_p<KP>, c.G, q, c, L.P, (size_t)c.n * KP, (const double*)L.R);
+  k_replace<KP><<<c.G, BLOCK, 0, q>>>(c, L.Q, L.R);
+  k_replace_p<KP><<<c.G, BLOCK, 0, q>>>(c, L.P, (size_t)c.n * KP, L.R);
 }
 
 template <int KP>
@@ -2176,14 +2115,12 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
           launch_round<KP>(c, cs, ce, csr, L, X, r, win, ell, q);
         }
       }
-      if (cudaError_t e = take_launch_error(); e != cudaSuccess) le = e;
       if (fused) {
         k_spmm_resid<KP><<<cs.G, BLOCK, 0, q>>>(cs, csr, B, X, L.Q);
         k_replace<KP><<<c.G, BLOCK, 0, q>>>(c, L.Q, L.R);
         k_update_xp<KP><<<c.G, BLOCK, 0, q>>>(c, SUM_REPLACE, X, L.P, L.R);
       } else {
         launch_check<KP>(c, cs, csr, L, B, X, q);
-        if (cudaError_t e = take_launch_error(); e != cudaSuccess) le = e;
       }
       if (fused) k_spmm_pq<KP><<<cs.G, BLOCK, 0, q>>>(cs, csr, L.P, L.Q, 1);
       cudaMemcpyAsync(h_sum, L.summary, sizeof(int) * SUM_N, cudaMemcpyDeviceToHost, q);

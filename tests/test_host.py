@@ -180,3 +180,17 @@ def test_install_rebinds_reference_entry_points():
         assert hg.Segmentation.locate is orig_loc
     finally:
         sys.path.remove(ref)
+
+
+def test_batch_width_policy():
+    """kp stays at the cap unless the SpMM's two-plane window (4 x bandwidth x kp
+    x 8 B) would exceed L2_WINDOW; never below 16, never above the column count."""
+    from types import SimpleNamespace
+
+    from paper_1811_07717_b200.device import PcgOperator
+
+    bw = lambda b: SimpleNamespace(bandwidth=b)  # noqa: E731
+    assert PcgOperator.batch_width(bw(12_232), 128, 64) == 64   # C2
+    assert PcgOperator.batch_width(bw(35_031), 256, 64) == 32   # C5
+    assert PcgOperator.batch_width(bw(10 ** 7), 256, 64) == 16  # floor
+    assert PcgOperator.batch_width(bw(100), 5, 64) == 5
