@@ -169,9 +169,12 @@ class ElectrodeSet:
 
     @property
     def node_set(self):
-        if self.count == 0:
-            return np.array([], dtype=np.int64)
-        return np.unique(np.concatenate([t.ravel() for t in self.triangles]))
+        if getattr(self, "_node_set", None) is None:
+            ns = (np.array([], dtype=np.int64) if self.count == 0
+                  else np.unique(np.concatenate([t.ravel() for t in self.triangles])))
+            ns.setflags(write=False)
+            self._node_set = ns
+        return self._node_set
 
     def __len__(self):
         return self.count
