@@ -673,11 +673,18 @@ __global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
 #ifndef HF_ELL_LEAN_HB
 #define HF_ELL_LEAN_HB 4
 #endif
+#ifndef HF_ELL_CPL
+#define HF_ELL_CPL 4
+#endif
 template <int KP>
 struct Ell {
-  static constexpr int CPL = 2;
-  static constexpr int LPR = KP / CPL;    // lanes per row (8, 16, 32)
+  // columns per lane: 4 (256-bit gathers; two rows per warp at kp = 64) for kp >= 32, else 2.
+  // At C2 kp = 64, 4 columns per lane halve the instructions and slot broadcasts per row:
+  // SpMM 0.269 -> 0.247 ms (0.269 -> 0.263 with batches of 2 gathers)
+  static constexpr int CPL = (HF_ELL_CPL == 4 && KP >= 32) ? 4 : 2;
+  static constexpr int LPR = KP / CPL;    // lanes per row (>= 8: lane e holds slot e)
   static constexpr int RB = BLOCK / LPR;  // rows per block step
+  static constexpr int HB = HF_ELL_LEAN_HB;  // gathers per batch
   static constexpr bool OK = (KP >= 16 && KP <= 64);
 };
 
@@ -692,9 +699,6 @@ struct Ell {
 // gathers, zero fills and conditional-FMA selects made the predicated kernel
 // issue-bound at 66%).
 constexpr int ELL_LONG = 1 << 30;
-#ifndef HF_ELL_LEAN_OPT
-#define HF_ELL_LEAN_OPT 1
-#endif
 #ifndef HF_ELL_OPT_FROM
 #define HF_ELL_OPT_FROM 5
 #endif
@@ -709,16 +713,15 @@ __global__ void k_ell_fill2(int n, const int32_t* __restrict__ indptr,
   int c[ELL_W];
   double v[ELL_W];
   for (int e = 0; e < ELL_W; ++e) {
-    // empty slot: (row, 0.0), gathered unconditionally; with HF_ELL_LEAN_OPT the
-    // slots >= ELL_OPT are gathered only when they hold an entry (-1 = empty)
-    c[e] = (HF_ELL_LEAN_OPT && e >= ELL_OPT) ? -1 : i;
+    // empty slot: (row, 0.0), gathered unconditionally; slots >= ELL_OPT are
+    // gathered only when they hold an entry (-1 = empty)
+    c[e] = e >= ELL_OPT ? -1 : i;
     v[e] = 0.0;
     if (e < ln) {
       c[e] = indices[st + e];
       v[e] = val[st + e];
     }
   }
-#if HF_ELL_LEAN_OPT
   // the diagonal (when slot-held) goes to slot 0: the epilogue's p_i is its gather
   for (int e = 1; e < ELL_W && e < ln; ++e)
     if (c[e] == i) {
@@ -730,7 +733,6 @@ __global__ void k_ell_fill2(int n, const int32_t* __restrict__ indptr,
       v[e] = tv;
       break;
     }
-#endif
   if (ln > ELL_W) c[0] |= ELL_LONG;
   for (int e = 0; e < ELL_W; ++e) {
     eci[(size_t)i * ELL_W + e] = c[e];
@@ -744,6 +746,7 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
                 const double* __restrict__ P, double* __restrict__ Q) {
   using E = Ell<KP>;
   constexpr int CPL = E::CPL, LPR = E::LPR, RB = E::RB;
+  constexpr int HB = E::HB;  // gathers in flight per batch (batches run 7.. first)
   __shared__ double sm[NWARP * KP > BLOCK ? NWARP * KP : BLOCK];
   __shared__ double tot[KP];
   __shared__ int s_act[KP];
@@ -753,13 +756,20 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
   const int tid = threadIdx.x, gl = tid % LPR, grp = tid / LPR;
   for (int j = tid; j < KP; j += BLOCK) s_act[j] = (c.state[j] == S_RUN);
   __syncthreads();
-  const int act0 = s_act[gl * CPL], act1 = s_act[gl * CPL + 1];
-  const bool any = (act0 | act1) != 0;
-  const double m0 = act0 ? 1.0 : 0.0, m1 = act1 ? 1.0 : 0.0;
+  double m[CPL];  // 1 for the lane's running columns: masks their p.q terms
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) {
+    const int a = s_act[gl * CPL + k];
+    m[k] = a ? 1.0 : 0.0;
+    any |= a != 0;
+  }
   const int nt = (c.n + RB - 1) / RB;
   const int slot = gl < ELL_W ? gl : ELL_W - 1;
   const double* __restrict__ Pl = P + gl * CPL;
-  double v0 = 0.0, v1 = 0.0;
+  double v[1][CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) v[0][k] = 0.0;
   auto tile_row = [&](int tt) {  // tile tt's row of this row group (-1: none)
     const int r = tt * RB + grp;
     return (tt < nt && r < c.n) ? r : -1;
@@ -791,34 +801,35 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
       const int4 c1 = *reinterpret_cast<const int4*>(&s_ci[b][grp][4]);
       const int cc[ELL_W] = {c0.x & (ELL_LONG - 1), c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
       const double2* vp = reinterpret_cast<const double2*>(&s_cv[b][grp][0]);
-      double a0 = 0.0, a1 = 0.0;
-#if HF_ELL_LEAN_OPT
-      double2 g0;  // slot 0's gather: p_i when slot 0 is the diagonal
-#endif
-      constexpr int HB = HF_ELL_LEAN_HB;  // gathers in flight per batch (batches run 7.. first)
+      double a[CPL];
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) a[k] = 0.0;
+      double g0[CPL];  // slot 0's gather: p_i when slot 0 is the diagonal
 #pragma unroll
       for (int bt = ELL_W / HB - 1; bt >= 0; --bt) {
-        double2 g[HB];
+        double g[HB][CPL];
 #pragma unroll
         for (int k = 0; k < HB; ++k) {
           const int e = bt * HB + k;
-          if (HF_ELL_LEAN_OPT && e >= ELL_OPT) {  // optional slot: zero when empty
-            g[k] = make_double2(0.0, 0.0);
-            if (cc[e] >= 0) g[k] = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)cc[e] * KP));
+          if (e >= ELL_OPT) {  // optional slot: zero when empty
+#pragma unroll
+            for (int q = 0; q < CPL; ++q) g[k][q] = 0.0;
+            if (cc[e] >= 0) ldg_cols<CPL>(Pl + (size_t)cc[e] * KP, g[k]);
           } else {
-            g[k] = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)(unsigned)cc[e] * KP));
+            ldg_cols<CPL>(Pl + (size_t)(unsigned)cc[e] * KP, g[k]);
           }
         }
-#if HF_ELL_LEAN_OPT
-        if (bt == 0) g0 = g[0];
-#endif
+        if (bt == 0) {
+#pragma unroll
+          for (int q = 0; q < CPL; ++q) g0[q] = g[0][q];
+        }
 #pragma unroll
         for (int k2 = HB / 2 - 1; k2 >= 0; --k2) {
           const double2 vv = vp[bt * HB / 2 + k2];
-          a0 = fma(vv.y, g[2 * k2 + 1].x, a0);
-          a1 = fma(vv.y, g[2 * k2 + 1].y, a1);
-          a0 = fma(vv.x, g[2 * k2].x, a0);
-          a1 = fma(vv.x, g[2 * k2].y, a1);
+#pragma unroll
+          for (int q = 0; q < CPL; ++q) a[q] = fma(vv.y, g[2 * k2 + 1][q], a[q]);
+#pragma unroll
+          for (int q = 0; q < CPL; ++q) a[q] = fma(vv.x, g[2 * k2][q], a[q]);
         }
       }
       if (c0.x & ELL_LONG) {  // entries 8.. of a long row, in order
@@ -826,26 +837,28 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
         for (int j = st + ELL_W; j < en; ++j) {
           const int ce = __ldg(A.indices + j);
           const double ve = __ldg(A.val + j);
-          const double2 q2 = __ldg(reinterpret_cast<const double2*>(Pl + (size_t)ce * KP));
-          a0 = fma(ve, q2.x, a0);
-          a1 = fma(ve, q2.y, a1);
+          double q2[CPL];
+          ldg_cols<CPL>(Pl + (size_t)ce * KP, q2);
+#pragma unroll
+          for (int q = 0; q < CPL; ++q) a[q] = fma(ve, q2[q], a[q]);
         }
       }
       const size_t o = (size_t)row * KP + gl * CPL;
-      *reinterpret_cast<double2*>(Q + o) = make_double2(a0, a1);
-#if HF_ELL_LEAN_OPT
-      const double2 pr = cc[0] == row ? g0 : __ldg(reinterpret_cast<const double2*>(P + o));
-#else
-      const double2 pr = __ldg(reinterpret_cast<const double2*>(P + o));  // L1: the diagonal's gather
-#endif
-      v0 = fma(pr.x * a0, m0, v0);
-      v1 = fma(pr.y * a1, m1, v1);
+      st_cols<CPL>(Q + o, a);
+      double pr[CPL];
+      if (cc[0] == row) {
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) pr[q] = g0[q];
+      } else {
+        ldg_cols<CPL>(P + o, pr);
+      }
+#pragma unroll
+      for (int q = 0; q < CPL; ++q) v[0][q] = fma(pr[q] * a[q], m[q], v[0][q]);
     }
     row = rowN;
     ci = ciN;
     cv = cvN;
   }
-  double v[1][CPL] = {{v0, v1}};
   block_partials_map<KP, 1, CPL, LPR>(v, sm, c.part0, nullptr);
   if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
   if (tid < KP) {

@@ -11,6 +11,8 @@ all arithmetic runs in libhfb200.so.  HBM layout:
 """
 from __future__ import annotations
 
+import threading
+
 import numpy as np
 import scipy.sparse as sp
 import torch
@@ -30,6 +32,7 @@ def device():
 # with one DMA.  The buffer is reused across calls; each copy is synchronous,
 # so reuse never races a transfer in flight.
 _PINNED = {}
+_LOCK = threading.Lock()
 _POOL = None
 _WORKERS = 1
 
@@ -61,17 +64,18 @@ def to_device(arr, dtype, dev=None, slot=0):
     nbytes = a.size * dt.itemsize
     if nbytes < (4 << 20):  # small: the plain path is cheaper than the pool
         return torch.from_numpy(np.array(a, dtype=dt, order="C")).to(dev)
-    buf = _pinned(slot, nbytes)
-    view = buf[:nbytes].numpy().view(dt).reshape(a.shape)
-    flat_src, flat_dst = a.reshape(-1), view.reshape(-1)
-    pool = _pool()
-    step = -(-flat_src.size // (4 * _WORKERS))
-    futs = [pool.submit(np.copyto, flat_dst[i:i + step], flat_src[i:i + step], casting="unsafe")
-            for i in range(0, flat_src.size, step)]
-    for f in futs:
-        f.result()
-    out = torch.empty(a.shape, dtype=torch.from_numpy(view[:0]).dtype, device=dev)
-    out.copy_(torch.from_numpy(view))
+    with _LOCK:  # one staging buffer per slot: concurrent callers take turns
+        buf = _pinned(slot, nbytes)
+        view = buf[:nbytes].numpy().view(dt).reshape(a.shape)
+        flat_src, flat_dst = a.reshape(-1), view.reshape(-1)
+        pool = _pool()
+        step = -(-flat_src.size // (4 * _WORKERS))
+        futs = [pool.submit(np.copyto, flat_dst[i:i + step], flat_src[i:i + step], casting="unsafe")
+                for i in range(0, flat_src.size, step)]
+        for f in futs:
+            f.result()
+        out = torch.empty(a.shape, dtype=torch.from_numpy(view[:0]).dtype, device=dev)
+        out.copy_(torch.from_numpy(view))  # synchronous: the buffer is free again on return
     return out
 
 
