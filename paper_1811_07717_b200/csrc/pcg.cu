@@ -676,12 +676,15 @@ __global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
 #ifndef HF_ELL_CPL
 #define HF_ELL_CPL 4
 #endif
+#ifndef HF_ELL_CPL4_MIN
+#define HF_ELL_CPL4_MIN 32  // smallest kp with 4-column lanes
+#endif
 template <int KP>
 struct Ell {
   // columns per lane: 4 (256-bit gathers; two rows per warp at kp = 64) for kp >= 32, else 2.
   // At C2 kp = 64, 4 columns per lane halve the instructions and slot broadcasts per row:
   // SpMM 0.269 -> 0.247 ms (0.269 -> 0.263 with batches of 2 gathers)
-  static constexpr int CPL = (HF_ELL_CPL == 4 && KP >= 32) ? 4 : 2;
+  static constexpr int CPL = (HF_ELL_CPL == 4 && KP >= HF_ELL_CPL4_MIN) ? 4 : 2;
   static constexpr int LPR = KP / CPL;    // lanes per row (>= 8: lane e holds slot e)
   static constexpr int RB = BLOCK / LPR;  // rows per block step
   static constexpr int HB = HF_ELL_LEAN_HB;  // gathers per batch
@@ -765,6 +768,9 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
     any |= a != 0;
   }
   const int nt = (c.n + RB - 1) / RB;
+  // slots per lane: a row group of LPR >= 8 lanes has lane e hold slot e; with
+  // LPR = 4 (kp 16, 4-column lanes) lane e holds slots e and e + 4
+  constexpr int SPL = LPR >= ELL_W ? 1 : ELL_W / LPR;
   const int slot = gl < ELL_W ? gl : ELL_W - 1;
   const double* __restrict__ Pl = P + gl * CPL;
   double v[1][CPL];
@@ -776,24 +782,32 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
   };
   int t = blockIdx.x;
   int row = tile_row(t);
-  int ci = 0;
-  double cv = 0.0;
-  if (row >= 0) {
-    ci = __ldg(eci + (size_t)row * ELL_W + slot);
-    cv = __ldg(ecv + (size_t)row * ELL_W + slot);
-  }
+  int ci[SPL];
+  double cv[SPL];
+  auto load_slots = [&](int r, int (&cs)[SPL], double (&vs)[SPL]) {
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      cs[k] = 0;
+      vs[k] = 0.0;
+      if (r >= 0) {
+        cs[k] = __ldg(eci + (size_t)r * ELL_W + slot + k * LPR);
+        vs[k] = __ldg(ecv + (size_t)r * ELL_W + slot + k * LPR);
+      }
+    }
+  };
+  load_slots(row, ci, cv);
   int b = 0;
   for (; t < nt; t += c.G, b ^= 1) {
     const int rowN = tile_row(t + c.G);
-    int ciN = 0;
-    double cvN = 0.0;
-    if (rowN >= 0) {  // next step's slots in flight during this one
-      ciN = __ldg(eci + (size_t)rowN * ELL_W + slot);
-      cvN = __ldg(ecv + (size_t)rowN * ELL_W + slot);
-    }
+    int ciN[SPL];
+    double cvN[SPL];
+    load_slots(rowN, ciN, cvN);  // next step's slots in flight during this one
     if (gl < ELL_W) {
-      s_ci[b][grp][gl] = ci;
-      s_cv[b][grp][gl] = cv;
+#pragma unroll
+      for (int k = 0; k < SPL; ++k) {
+        s_ci[b][grp][gl + k * LPR] = ci[k];
+        s_cv[b][grp][gl + k * LPR] = cv[k];
+      }
     }
     __syncwarp();
     if (row >= 0 && any) {
@@ -856,8 +870,11 @@ __global__ void __launch_bounds__(BLOCK, HF_ELL_BPS)
       for (int q = 0; q < CPL; ++q) v[0][q] = fma(pr[q] * a[q], m[q], v[0][q]);
     }
     row = rowN;
-    ci = ciN;
-    cv = cvN;
+#pragma unroll
+    for (int k = 0; k < SPL; ++k) {
+      ci[k] = ciN[k];
+      cv[k] = cvN[k];
+    }
   }
   block_partials_map<KP, 1, CPL, LPR>(v, sm, c.part0, nullptr);
   if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
