@@ -220,6 +220,7 @@ def run_ours(args):
     from paper_1811_07717_b200 import _native as N
     from paper_1811_07717_b200 import synthetic
     from paper_1811_07717_b200.distributed import init_from_env, sharded_leadfield
+    from paper_1811_07717_b200.device import to_host
     from paper_1811_07717_b200.engine import EegEngine, column_blocks
     from paper_1811_07717_b200.solver import PcgConfig
 
@@ -280,10 +281,13 @@ def run_ours(args):
         w0 = time.perf_counter()
         for _ in range(args.steps):
             eng2 = make_engine(prob.sources)  # G' assembled on the device inside the timed call
-            lf_dev = eng2.build() if world == 1 else sharded_leadfield(eng2, world, rank)
+            if world == 1:
+                lf_host = eng2.build(to_host=True)
+            else:
+                lf_dev = sharded_leadfield(eng2, world, rank)
+                lf_host = None if lf_dev is None else to_host(lf_dev.contiguous())
             h2d += eng2.h2d_bytes
-            if lf_dev is not None:
-                lf_host = lf_dev.cpu().numpy()
+            if lf_host is not None:
                 d2h += lf_host.nbytes + 8 * L * L
             del eng2
         torch.cuda.synchronize()
@@ -299,7 +303,7 @@ def run_ours(args):
         e2e = {"value": L * args.steps / wall, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d / args.steps), "d2h_bytes_per_step": int(d2h / args.steps),
                "ms_per_step": round(wall * 1e3 / args.steps, 2),
-               "api": "engine.EegEngine(mesh, electrodes, sources).build() -> LF on host "
+               "api": "engine.EegEngine(mesh, electrodes, sources).build(to_host=True) -> LF on host "
                       "(G' assembled on the device inside the step)"}
 
     roof = None

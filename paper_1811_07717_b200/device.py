@@ -56,6 +56,20 @@ def _pinned(slot, nbytes):
     return buf
 
 
+def to_host(t, slot=7):
+    """Copy a device tensor to a new host numpy array through pinned staging
+    (one DMA at full PCIe rate instead of a pageable copy)."""
+    nbytes = t.numel() * t.element_size()
+    if nbytes < (4 << 20):
+        return t.cpu().numpy()
+    with _LOCK:
+        buf = _pinned(slot, nbytes)
+        stage = torch.from_numpy(buf[:nbytes].numpy().view(np.dtype(str(t.dtype).replace("torch.", ""))))
+        stage = stage.view(t.shape)
+        stage.copy_(t)  # synchronous device -> pinned copy
+        return stage.numpy().copy()
+
+
 def to_device(arr, dtype, dev=None, slot=0):
     """Copy a host array to a new device tensor of numpy dtype `dtype` via pinned staging."""
     dev = dev or device()

@@ -24,6 +24,7 @@ import torch
 
 from . import model
 from .device import DeviceCsr, PcgOperator, device, to_device
+from .device import to_host as _to_host
 from .fem import DeviceMesh, assemble_device, blocks_device
 from .leadfield import lf_tail_device, response_block_device, response_operator, symmetrize
 from .solver import PcgConfig, _raise_failed, rhs_block, solve_block
@@ -146,7 +147,7 @@ class EegEngine:
         M = symmetrize(self.response_block(T).cpu().numpy())
         W = response_operator(M, self.R)
         LF = self.lf_partial(T, W)
-        return LF.cpu().numpy() if to_host else LF
+        return _to_host(LF.contiguous()) if to_host else LF
 
 
 def eeg_leadfield_from_mesh(mesh, electrodes, sources, cfg=PcgConfig()):

@@ -87,3 +87,28 @@ def test_c2_scale_generate_mesh_consistent(mg):
     nl = mg.locate(seg, mesh.nodes)[mesh.tetra]
     plain = np.all((nl == nl[:, :1]) | (nl < 0), axis=1)
     np.testing.assert_array_equal(mesh.labels[plain], cl[plain])
+
+
+def test_segmentation_to_leadfield_matches_reference(mg):
+    """Segmentation -> generate_mesh (device) -> EEG lead field (device), against the
+    reference's lead field for the same segmentation (sphere_small: icosphere(0.1, 2),
+    h = 0.045; tests/golden/make_golden.py:149-163)."""
+    import paper_1811_07717_b200 as eng
+    from paper_1811_07717_b200 import model
+    from paper_1811_07717_b200.geometry import Compartment, Segmentation, icosphere
+
+    from tests.fixtures import electrodes_from_fixture
+
+    fx = load("sphere_small.npz")
+    mesh = mg.generate_mesh(Segmentation([Compartment(icosphere(0.1, 2), 0.33, active=True)]), 0.045)
+    np.testing.assert_array_equal(mesh.tetra, fx["tetra"])
+    el = electrodes_from_fixture(mesh, fx)
+    B, C, R = model.assemble_B_C_R(mesh, el)
+    src = model.SourceSpace(positions=fx["src_positions"], orientations=None,
+                            element_ids=fx["src_elements"], mode="unconstrained")
+    G = model.assemble_G(mesh, src)
+    sysm = model.CemSystem(mesh=mesh, electrodes=el, A=eng.assemble_A(mesh, el), B=B, C=C, R=R,
+                           ground=model.ground_node(mesh, el), G=G, source_space=src)
+    lf = eng.eeg_leadfield(sysm, eng.PcgConfig(tolerance=float(fx["tol"])))
+    ref = fx["LF"]
+    assert np.linalg.norm(lf.matrix - ref) / np.linalg.norm(ref) <= 1e-6

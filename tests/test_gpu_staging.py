@@ -20,3 +20,20 @@ def test_to_device_exact(cuda, shape, src, dst):
         np.testing.assert_array_equal(t.cpu().numpy(), a.astype(dst))
     b = a[::2]  # non-contiguous source
     np.testing.assert_array_equal(to_device(b, dst).cpu().numpy(), b.astype(dst))
+
+
+@pytest.mark.parametrize("shape", [(128, 30000), (7,)])
+def test_to_host_exact(cuda, shape):
+    import torch
+
+    from paper_1811_07717_b200.device import to_host
+
+    t = torch.randn(shape, dtype=torch.float64, device="cuda")
+    for _ in range(2):
+        h = to_host(t)
+        assert isinstance(h, np.ndarray) and h.shape == tuple(shape)
+        np.testing.assert_array_equal(h, t.cpu().numpy())
+    h0 = to_host(t)
+    t.add_(1.0)
+    h1 = to_host(t)
+    assert not np.shares_memory(h0, h1) and np.all(h1 == h0 + 1.0)
