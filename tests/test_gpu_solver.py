@@ -301,3 +301,21 @@ class TestTransferMatrix:
             got.append(exc.value)
         np.testing.assert_array_equal(got[0].best_x, got[1].best_x)
         assert got[0].column == got[1].column and got[0].residual == got[1].residual
+
+
+def test_csr_bandwidth_and_batch_width(cuda):
+    """hf_csr_bandwidth = max_i max(i - first col, last col - i) of the SpMM copy;
+    the batch width follows it (PcgOperator.batch_width)."""
+    import scipy.sparse as sp
+
+    from paper_1811_07717_b200.device import DeviceCsr, PcgOperator
+
+    rng = np.random.default_rng(5)
+    n = 2000
+    M = sp.random(n, n, density=0.002, random_state=rng, format="csr")
+    A = (M + M.T + sp.diags(np.full(n, 10.0))).tocsr()
+    A.sort_indices()
+    ref = max(max(i - A.indices[A.indptr[i]], A.indices[A.indptr[i + 1] - 1] - i) for i in range(n))
+    op = PcgOperator(DeviceCsr.from_scipy(A))
+    assert op.bandwidth == ref
+    assert op.batch_width(128, 64) == 64  # a 2000-row window is far below L2
