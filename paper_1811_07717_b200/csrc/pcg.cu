@@ -676,6 +676,9 @@ __global__ void __launch_bounds__(BLOCK, Spmm<KP>::BPS)
 #ifndef HF_ELL_CPL
 #define HF_ELL_CPL 4
 #endif
+#ifndef HF_ELL_MAXKP
+#define HF_ELL_MAXKP 64  // widest batch served by the ELL kernel (128: 4-column lanes, one row per warp)
+#endif
 #ifndef HF_ELL_CPL4_MIN
 #define HF_ELL_CPL4_MIN 32  // smallest kp with 4-column lanes
 #endif
@@ -688,7 +691,7 @@ struct Ell {
   static constexpr int LPR = KP / CPL;    // lanes per row (>= 8: lane e holds slot e)
   static constexpr int RB = BLOCK / LPR;  // rows per block step
   static constexpr int HB = HF_ELL_LEAN_HB;  // gathers per batch
-  static constexpr bool OK = (KP >= 16 && KP <= 64);
+  static constexpr bool OK = (KP >= 16 && KP <= HF_ELL_MAXKP);
 };
 
 // The ELL copy is built so that slots can be gathered and multiplied

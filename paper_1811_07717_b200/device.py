@@ -157,7 +157,8 @@ def ldp_device(A: DeviceCsr):
     return d, int(nz.value)
 
 
-L2_WINDOW = 48 << 20  # bytes of the 126 MB L2 the SpMM's two-plane reuse window may take
+# bytes of the 126 MB L2 the SpMM's two-plane reuse window may take (HFB200_L2_WINDOW_MB: experiments)
+L2_WINDOW = int(float(__import__("os").environ.get("HFB200_L2_WINDOW_MB", "48")) * (1 << 20))
 
 
 class PcgOperator:
