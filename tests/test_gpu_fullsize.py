@@ -81,3 +81,46 @@ def test_c2_leadfield_properties(c2):
     assert np.all(info.true_residual <= TOL)
     n = 1_001_184
     assert np.all(info.iterations > 0) and np.all(info.iterations < int(5 * np.sqrt(n)) + 1000)
+
+
+def test_c4_eit_leadfield_sampled_against_oracle(c2):
+    """C4 (BASELINE.json configs[3]) on the C2 mesh: 64 electrodes, 32 adjacent-pair
+    patterns, 5,000 DOFs.  DOF sets identical to the exact host k-d-tree path
+    (leadfield.py:80-101), sampled sensitivity columns vs the oracle's
+    _dof_sensitivities (leadfield.py:179-207), zero-mean pattern blocks."""
+    import torch
+
+    import oracle
+    from paper_1811_07717_b200 import model, synthetic
+    from paper_1811_07717_b200.leadfield import (
+        _electrode_response_device, _solve_response, adjacent_pair_patterns, build_dof_map,
+        dof_sensitivities_device, eit_leadfield)
+    from paper_1811_07717_b200.solver import PcgConfig, solve_block
+
+    mesh = c2["prob"].mesh
+    el = model.ElectrodeSet.from_centers(mesh, synthetic.fibonacci_sphere_points(64, 0.092),
+                                         radius=0.012, impedances=1e3)
+    dofs = build_dof_map(mesh, [0, 1], 5000, seed=2, method="device")
+    tree = build_dof_map(mesh, [0, 1], 5000, seed=2, method="tree")
+    assert all(np.array_equal(a, b) for a, b in zip(dofs.element_sets, tree.element_sets))
+    I = adjacent_pair_patterns(64)[:, :32]
+    B, C, R = model.assemble_B_C_R(mesh, el)
+    from paper_1811_07717_b200.fem import assemble_A
+
+    A = assemble_A(mesh, el)
+    sysm = model.CemSystem(mesh=mesh, electrodes=el, A=A, B=B, C=C, R=R,
+                           ground=model.ground_node(mesh, el))
+    cfg = PcgConfig(TOL)
+    lf = eit_leadfield(sysm, dofs, I, cfg)
+    assert lf.matrix.shape == (32 * 64, 5000) and np.isfinite(lf.matrix).all()
+    blocks = lf.matrix.reshape(32, 64, -1)
+    assert np.abs(blocks.sum(axis=1)).max() <= 1e-10 * np.abs(lf.matrix).max()
+    dsys, T, M, _ = _electrode_response_device(sysm, cfg)
+    V = _solve_response(M, I)
+    U, _ = solve_block(dsys.op, dsys.Bd @ torch.from_numpy(np.ascontiguousarray(V)).cuda(), cfg)
+    Q = dof_sensitivities_device(mesh, dofs, sysm.ground, T, U, 64, 32)
+    pick = [0, 1234, 4999]
+    Qo = oracle.dof_sensitivities(mesh.nodes, mesh.tetra, [dofs.element_sets[k] for k in pick],
+                                  sysm.ground, U.cpu().numpy(), T.cpu().numpy())
+    Qg = Q[:, pick, :].cpu().numpy()
+    assert np.linalg.norm(Qg - Qo) / np.linalg.norm(Qo) < 1e-12
