@@ -11,11 +11,10 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-# HFB200_LIB selects an experimental build (python paper_1811_07717_b200/build.py --variant ...)
-LIB_PATH = os.environ.get("HFB200_LIB") or os.path.join(_HERE, "_lib", "libhfb200.so")
+LIB_PATH = os.path.join(_HERE, "_lib", "libhfb200.so")
 
 HF_COL_DONE, HF_COL_FAILED, HF_COL_ZERO, HF_COL_FROZEN = 2, 3, 4, 5
-PCG_WIDTHS = (2, 4, 8, 16, 32, 64, 128)
+PCG_WIDTHS = (2, 4, 8, 16, 32, 64)
 
 
 class HfCsr(C.Structure):

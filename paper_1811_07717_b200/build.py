@@ -35,17 +35,16 @@ def stale():
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force=False, verbose=False, defines=(), out=None):
-    """Compile libhfb200.so; `defines` (-DNAME=V) with `out` build an experimental
-    variant elsewhere (loaded with HFB200_LIB=path)."""
-    out = out or LIB
-    if out == LIB and not force and not stale():
+def build(force=False, verbose=False):
+    """Compile libhfb200.so (one code path: no build variants, no runtime switches)."""
+    out = LIB
+    if not force and not stale():
         return LIB
     os.makedirs(os.path.dirname(out), exist_ok=True)
     tmp = out + ".tmp"
     cmd = [nvcc_path(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-shared",
            "-Xcompiler", "-fPIC", "-Xptxas", "-v" if verbose else "-O3",
-           "-I", os.path.join(ROOT, "include"), *defines,
+           "-I", os.path.join(ROOT, "include"),
            *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
@@ -57,12 +56,5 @@ def build(force=False, verbose=False, defines=(), out=None):
 
 
 if __name__ == "__main__":
-    args = sys.argv[1:]
-    if "--variant" in args:  # build.py --variant NAME -DX=1 ...
-        name = args[args.index("--variant") + 1]
-        defs = [a for a in args if a.startswith("-D")]
-        print(build(force=True, verbose="-v" in args, defines=defs,
-                    out=os.path.join(LIBDIR, "variants", f"libhfb200_{name}.so")))
-    else:
-        build(force=True, verbose="-v" in args)
-        print(LIB)
+    build(force=True, verbose="-v" in sys.argv[1:])
+    print(LIB)

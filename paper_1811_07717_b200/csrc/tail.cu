@@ -6,6 +6,8 @@
 //                    column), then multiplied by W = -R M^-1 on the fp64 tensor
 //                    path (DMMA: mma.sync.m8n8k4.f64).   (leadfield.py:128-129)
 //   k_eit_sens       per-DOF sensitivities Q[p, m, :] = T' K_m u_p  (leadfield.py:179-207)
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace hf {
@@ -96,9 +98,6 @@ __global__ void __launch_bounds__(LF_THREADS)
 
 // ---------------------------------------------------------------- EIT sensitivities
 constexpr int ES_THREADS = 256;
-constexpr int ES_EB = 8;         // elements staged per batch
-constexpr int ES_MAXO = 16;      // outputs per thread per CTA (P*L chunk <= 4096)
-constexpr int ES_CHUNK = ES_THREADS * ES_MAXO;
 
 #define MUL(a, b) __dmul_rn((a), (b))
 #define ADD(a, b) __dadd_rn((a), (b))
@@ -138,72 +137,111 @@ __device__ void unit_block(const double* __restrict__ nodes, const int32_t* __re
     }
 }
 
-__global__ void __launch_bounds__(ES_THREADS)
+// Q_m (P x L) = S' Tg over the DOF's element corners k = (e, i):
+//   S[k, p]  = sum_j K_e[i, j] u[conn_ej, p]     (einsum "eij,ej->ei", leadfield.py:203)
+//   Tg[k, l] = T[conn_ei, l]                      (T[conn], leadfield.py:198)
+// i.e. np.add.at(Q[p], owner, Tg' s) (leadfield.py:204-206) as one GEMM with
+// K = 4 |E_m| per DOF, run on the fp64 tensor pipe (DMMA m8n8k4).  One CTA per
+// (DOF, block of <= 64 electrode columns, block of <= 64 patterns); elements in
+// chunks of ES_EC: per chunk the CTA computes the unit-sigma blocks, gathers the
+// chunk's U and T rows into shared memory, forms S, and every warp accumulates
+// its 8x8 output tiles with DMMA.  Shared rows are padded to a stride = 4 mod 16
+// doubles so the A/B fragment loads are bank-conflict free.
+constexpr int ES_EC = 16;             // elements per chunk -> K = 64 per chunk
+constexpr int ES_K = 4 * ES_EC;
+constexpr int ES_MAXP = 64, ES_MAXL = 64;
+constexpr int ES_WARPS = ES_THREADS / 32;
+constexpr int ES_MAXT = (ES_MAXP / 8) * (ES_MAXL / 8) / ES_WARPS;  // output tiles per warp
+
+__host__ __device__ inline int es_stride(int w) { return ((w + 7) / 8) * 8 + ((((w + 7) / 8) * 8) % 16 == 0 ? 4 : 12); }
+
+__global__ void __launch_bounds__(ES_THREADS, 2)
     k_eit_sens(const double* __restrict__ nodes, const int32_t* __restrict__ tetra,
                const int32_t* __restrict__ dof_elems, const int32_t* __restrict__ dof_ptr,
                int n_dofs, int ground, const double* __restrict__ T, int ldt, int L,
                const double* __restrict__ U, int ldu, int P, double* __restrict__ Q) {
   extern __shared__ double sh[];
-  double* sT = sh;                         // [EB][4][L]
-  double* sS = sT + ES_EB * 4 * L;         // [EB][4][P]
-  double* sK = sS + ES_EB * 4 * P;         // [EB][16]
-  double* sU = sK + ES_EB * 16;            // [EB][4][P]
-  __shared__ int32_t sC[ES_EB][4];
   const int m = blockIdx.x;
-  const int o0 = blockIdx.y * ES_CHUNK;
-  const int PL = P * L;
-  const int tid = threadIdx.x;
-  double acc[ES_MAXO];
+  const int l0 = blockIdx.y * ES_MAXL, p0 = blockIdx.z * ES_MAXP;
+  const int nl = min(ES_MAXL, L - l0), np_ = min(ES_MAXP, P - p0);
+  const int SP = es_stride(np_), SL = es_stride(nl);
+  double* sS = sh;                      // [ES_K][SP]
+  double* sT = sS + ES_K * SP;          // [ES_K][SL]
+  double* sU = sT + ES_K * SL;          // [ES_K][np_]
+  double* sK = sU + ES_K * np_;         // [ES_EC][16]
+  __shared__ int32_t sC[ES_EC][4];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, t4 = lane & 3;
+  const int MT = (np_ + 7) / 8, NTt = (nl + 7) / 8, ntile = MT * NTt;
+  double acc[ES_MAXT][2];
 #pragma unroll
-  for (int k = 0; k < ES_MAXO; ++k) acc[k] = 0.0;
+  for (int j = 0; j < ES_MAXT; ++j) acc[j][0] = acc[j][1] = 0.0;
   const int e0 = dof_ptr[m], e1 = dof_ptr[m + 1];
-  for (int eb = e0; eb < e1; eb += ES_EB) {
-    const int ne = min(ES_EB, e1 - eb);
-    if (tid < ne * 4) {
-      const int e = dof_elems[eb + tid / 4];
-      sC[tid / 4][tid % 4] = tetra[4 * (size_t)e + (tid % 4)];
+  for (int eb = e0; eb < e1; eb += ES_EC) {
+    const int ne = min(ES_EC, e1 - eb);
+    if (tid < ES_EC * 4) {
+      const int e = tid / 4;
+      sC[e][tid % 4] = e < ne ? tetra[4 * (size_t)dof_elems[eb + e] + (tid % 4)] : -1;
     }
     __syncthreads();
     if (tid < ne) unit_block(nodes, sC[tid], ground, sK + 16 * tid);
-    for (int o = tid; o < ne * 4 * L; o += ES_THREADS) {
-      const int l = o % L, ei = o / L;
-      sT[o] = __ldg(T + (size_t)sC[ei / 4][ei % 4] * ldt + l);
+    for (int o = tid; o < ES_K * np_; o += ES_THREADS) {  // U rows of the chunk's corners
+      const int k = o / np_, p = o % np_;
+      const int node = sC[k / 4][k % 4];
+      sU[o] = node >= 0 ? __ldg(U + (size_t)node * ldu + p0 + p) : 0.0;
     }
-    for (int o = tid; o < ne * 4 * P; o += ES_THREADS) {
-      const int p = o % P, ei = o / P;
-      sU[o] = __ldg(U + (size_t)sC[ei / 4][ei % 4] * ldu + p);
-    }
-    __syncthreads();
-    // s[e,i,p] = sum_j K_e[i,j] u[conn_ej, p]   (einsum "eij,ej->ei")
-    for (int o = tid; o < ne * 4 * P; o += ES_THREADS) {
-      const int p = o % P, ei = o / P, e = ei / 4, i = ei % 4;
-      const double* K = sK + 16 * e + 4 * i;
-      const double* u = sU + (size_t)e * 4 * P + p;
-      sS[o] = K[0] * u[0] + K[1] * u[P] + K[2] * u[2 * P] + K[3] * u[3 * P];
+    for (int o = tid; o < ES_K * nl; o += ES_THREADS) {  // T rows of the chunk's corners
+      const int k = o / nl, l = o % nl;
+      const int node = sC[k / 4][k % 4];
+      sT[k * SL + l] = node >= 0 ? __ldg(T + (size_t)node * ldt + l0 + l) : 0.0;
     }
     __syncthreads();
-    // contrib[p, l] = sum_i T[conn_ei, l] s[e,i,p]; Q[p, m, l] += contrib (np.add.at order)
-    for (int e = 0; e < ne; ++e) {
-#pragma unroll
-      for (int k = 0; k < ES_MAXO; ++k) {
-        const int o = o0 + tid + k * ES_THREADS;
-        if (o < PL) {
-          const int p = o / L, l = o % L;
-          const double* tt = sT + (size_t)e * 4 * L + l;
-          const double* ss = sS + (size_t)e * 4 * P + p;
-          const double contrib = tt[0] * ss[0] + tt[L] * ss[P] + tt[2 * L] * ss[2 * P] + tt[3 * L] * ss[3 * P];
-          acc[k] += contrib;
-        }
+    for (int o = tid; o < ES_K * np_; o += ES_THREADS) {  // S = K_e u_e
+      const int k = o / np_, p = o % np_, e = k / 4, i = k % 4;
+      double v = 0.0;
+      if (e < ne) {
+        const double* K = sK + 16 * e + 4 * i;
+        const double* u = sU + (size_t)(4 * e) * np_ + p;
+        v = K[0] * u[0];
+        v = fma(K[1], u[np_], v);
+        v = fma(K[2], u[2 * np_], v);
+        v = fma(K[3], u[3 * np_], v);
       }
+      sS[k * SP + p] = v;
+    }
+    // zero the padded output rows/columns' operands (p >= np_, l >= nl) once per chunk
+    for (int o = tid; o < ES_K * (MT * 8 - np_); o += ES_THREADS) {
+      const int w = MT * 8 - np_;
+      sS[(o / w) * SP + np_ + o % w] = 0.0;
+    }
+    for (int o = tid; o < ES_K * (NTt * 8 - nl); o += ES_THREADS) {
+      const int w = NTt * 8 - nl;
+      sT[(o / w) * SL + nl + o % w] = 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < ES_MAXT; ++j) {
+      const int ti = warp + ES_WARPS * j;
+      if (ti >= ntile) break;
+      const int mt = ti % MT, nt = ti / MT;
+      const double* ap = sS + (size_t)t4 * SP + mt * 8 + g;  // A[row p][k] = S[k][p]
+      const double* bp = sT + (size_t)t4 * SL + nt * 8 + g;  // B[k][col l] = Tg[k][l]
+#pragma unroll 4
+      for (int k0 = 0; k0 < ES_K; k0 += 4)
+        dmma_8x8x4(acc[j][0], acc[j][1], ap[(size_t)k0 * SP], bp[(size_t)k0 * SL]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int k = 0; k < ES_MAXO; ++k) {
-    const int o = o0 + tid + k * ES_THREADS;
-    if (o < PL) {
-      const int p = o / L, l = o % L;
-      Q[((size_t)p * n_dofs + m) * L + l] = acc[k];
+  for (int j = 0; j < ES_MAXT; ++j) {
+    const int ti = warp + ES_WARPS * j;
+    if (ti >= ntile) break;
+    const int mt = ti % MT, nt = ti / MT;
+    const int p = mt * 8 + g, l = nt * 8 + 2 * t4;
+    if (p < np_) {
+      double* q = Q + ((size_t)(p0 + p) * n_dofs + m) * L + l0;
+      if (l < nl) q[l] = acc[j][0];
+      if (l + 1 < nl) q[l + 1] = acc[j][1];
     }
   }
 }
@@ -290,16 +328,12 @@ extern "C" int hf_eit_sens(const double* nodes, const int32_t* tetra, const int3
   }
   if (n_dofs == 0) return HF_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const size_t smem = sizeof(double) * (tail::ES_EB * 4 * (size_t)L + tail::ES_EB * 4 * (size_t)P * 2 +
-                                        tail::ES_EB * 16);
-  if (smem > 200 * 1024) {
-    set_error("hf_eit_sens: L=%d, P=%d exceed the shared-memory tile", L, P);
-    return HF_ERR_ARG;
-  }
+  const int nl = std::min(L, tail::ES_MAXL), np_ = std::min(P, tail::ES_MAXP);
+  const size_t smem = sizeof(double) * ((size_t)tail::ES_K * (tail::es_stride(np_) + tail::es_stride(nl) + np_) +
+                                        16 * tail::ES_EC);
   HF_CUDA(cudaFuncSetAttribute(tail::k_eit_sens, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem));
-  const int chunks = (P * L + tail::ES_CHUNK - 1) / tail::ES_CHUNK;
-  dim3 grid(n_dofs, chunks);
+  dim3 grid(n_dofs, (L + tail::ES_MAXL - 1) / tail::ES_MAXL, (P + tail::ES_MAXP - 1) / tail::ES_MAXP);
   tail::k_eit_sens<<<grid, tail::ES_THREADS, smem, s>>>(nodes, tetra, dof_elems, dof_ptr, n_dofs,
                                                         ground, T, ldt, L, U, ldu, P, Q);
   HF_LAUNCH_CHECK();

@@ -14,9 +14,11 @@ exchanges are small:
 `sharded_eit_leadfield` adds the EIT pattern solves, sharded by pattern, and
 one all-gather of U (n x P); see its docstring.
 
-Iterates of a column never depend on which rank or batch solves it, so the
-transfer columns are bit-identical to the single-GPU build; only the final
-sum over ranks changes the LF at rounding level.
+A column's iterates never depend on which rank or batch solves it (the
+solver's reductions are canonical, pcg.cu), so the transfer columns are
+bit-identical to the single-GPU build; only the final sum over ranks changes
+the LF at rounding level.  A convergence failure on any rank is raised on
+every rank, before the next collective, as the same ConvergenceError.
 
 `sharded_leadfield` only uses the engine's stage methods and torch.distributed
 collectives, so the same orchestration runs with NCCL on GPUs and with gloo on
@@ -38,23 +40,87 @@ def sharded_leadfield(engine, world=None, rank=None, group=None):
     L = engine.L
     blocks = column_blocks(L, world)
     A = engine.assemble()
-    T = engine.solve(A)
+    T = _solve_consistently(lambda: engine.solve(A), engine.c0, L, blocks, group, tag=True)
     Mraw = _all_gather_columns(engine.response_block(T), blocks, group)  # L x L
     M = symmetrize(Mraw.cpu().numpy())
     W = response_operator(M, engine.R)
     LFp = engine.lf_partial(T, W).contiguous()
-    dist.reduce(LFp, dst=0, op=dist.ReduceOp.SUM, group=group)
+    _reduce_sum(LFp, group)
     return LFp if rank == 0 else None
+
+
+def _host_collectives(group):
+    """gloo moves CPU tensors only: stage device tensors through the host for it."""
+    return dist.get_backend(group) == "gloo"
+
+
+def _reduce_sum(X, group):
+    if _host_collectives(group) and X.is_cuda:
+        h = X.cpu()
+        dist.reduce(h, dst=0, op=dist.ReduceOp.SUM, group=group)
+        X.copy_(h)
+    else:
+        dist.reduce(X, dst=0, op=dist.ReduceOp.SUM, group=group)
 
 
 def _all_gather_columns(X, blocks, group):
     """Concatenate the column blocks every rank holds (padded to equal width for the collective)."""
     width = max(c1 - c0 for c0, c1 in blocks)
-    pad = torch.zeros((X.shape[0], width), dtype=X.dtype, device=X.device)
-    pad[:, :X.shape[1]] = X
+    dev = "cpu" if _host_collectives(group) else X.device
+    pad = torch.zeros((X.shape[0], width), dtype=X.dtype, device=dev)
+    pad[:, :X.shape[1]] = X.to(dev)
     parts = [torch.empty_like(pad) for _ in blocks]
     dist.all_gather(parts, pad, group=group)
-    return torch.cat([p[:, :c1 - c0] for p, (c0, c1) in zip(parts, blocks)], dim=1)
+    return torch.cat([p[:, :c1 - c0] for p, (c0, c1) in zip(parts, blocks)], dim=1).to(X.device)
+
+
+def _solve_consistently(solve, c0, n_cols, blocks, group, tag):
+    """Run this rank's solve; if any rank's columns fail, every rank raises the same
+    ConvergenceError before the next collective (the reference's transfer_matrix
+    reports the first failing column in index order, solver.py:129-136): the
+    lowest failing global column wins, and its owner broadcasts best_x."""
+    from .errors import ConvergenceError
+
+    err, X = None, None
+    try:
+        X = solve()
+    except ConvergenceError as exc:
+        err = exc
+    mine = n_cols if err is None else c0 + int(getattr(err, "local_column", 0))
+    first = mine
+    flag = torch.tensor([first], dtype=torch.int64)
+    if not _host_collectives(group):
+        flag = flag.cuda()
+    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+    first = int(flag.item())
+    if first >= n_cols:
+        return X
+    owner = next(r for r, (b0, b1) in enumerate(blocks) if b0 <= first < b1)
+    meta = torch.zeros(3, dtype=torch.float64)
+    n = None
+    if err is not None and mine == first:
+        n = len(err.best_x)
+        meta[:] = torch.tensor([float(n), float(err.residual), float(err.iterations)])
+    if not _host_collectives(group):
+        meta = meta.cuda()
+    dist.broadcast(meta, src=_global_rank(owner, group), group=group)
+    n, residual, iters = int(meta[0].item()), float(meta[1].item()), int(meta[2].item())
+    best = torch.zeros(n, dtype=torch.float64)
+    if err is not None and mine == first:
+        best = torch.from_numpy(err.best_x.copy())
+    if not _host_collectives(group):
+        best = best.cuda()
+    dist.broadcast(best, src=_global_rank(owner, group), group=group)
+    out = ConvergenceError(str(err) if err is not None else
+                           f"PCG did not converge in column {first} (rank {owner})",
+                           best_x=best.cpu().numpy(), residual=residual, iterations=iters)
+    if tag:
+        out.column = first
+    raise out
+
+
+def _global_rank(r, group):
+    return r if group is None else dist.get_global_rank(group, r)
 
 
 def sharded_eit_leadfield(engine, dofs, currents, world=None, rank=None, group=None):
@@ -78,20 +144,23 @@ def sharded_eit_leadfield(engine, dofs, currents, world=None, rank=None, group=N
     I = check_current_patterns(currents, L)
     P = I.shape[1]
     A = engine.assemble()
-    T = engine.solve(A)
+    T = _solve_consistently(lambda: engine.solve(A), engine.c0, L, column_blocks(L, world), group,
+                            tag=True)
     Mraw = _all_gather_columns(engine.response_block(T), column_blocks(L, world), group)
     M = symmetrize(Mraw.cpu().numpy())
     W = response_operator(M, engine.R)
     V = _solve_response(M, I)                                  # L x P
     pblocks = column_blocks(P, world)
     p0, p1 = pblocks[rank]
-    if p1 > p0:
-        Ub = engine.solve_rhs(A, np.asarray(engine.B @ V[:, p0:p1]))  # n x Pb
-    else:  # more ranks than patterns
-        Ub = T.new_zeros((T.shape[0], 0))
+    def solve_u():
+        if p1 > p0:
+            return engine.solve_rhs(A, np.asarray(engine.B @ V[:, p0:p1]))  # n x Pb
+        return T.new_zeros((T.shape[0], 0))  # more ranks than patterns
+    # pattern solves follow pcg_solve's semantics (leadfield.py:227): no column tag
+    Ub = _solve_consistently(solve_u, p0, P, pblocks, group, tag=False)
     U = _all_gather_columns(Ub, pblocks, group)
     cols = engine.eit_partial(dofs, T, U, W).contiguous()      # P*L x n_dofs
-    dist.reduce(cols, dst=0, op=dist.ReduceOp.SUM, group=group)
+    _reduce_sum(cols, group)
     if rank != 0:
         return None
     return LeadField(matrix=cols.cpu().numpy(), positions=dofs.centers, orientations=None,

@@ -51,7 +51,7 @@ class EegEngine:
         dev = dev or device()
         self.cfg = cfg
         self.h2d_bytes = 0
-        self.dmesh = DeviceMesh(mesh.nodes, mesh.tetra, dev)
+        self.dmesh = DeviceMesh.of(mesh)  # once per mesh object (G' assembly reuses it)
         self.h2d_bytes += self.dmesh.nodes.numel() * 8 + self.dmesh.tetra.numel() * 4
         self.sigma = to_device(mesh.sigma, np.float64, dev, slot=2)
         self.h2d_bytes += self.sigma.numel() * 8
@@ -109,8 +109,13 @@ class EegEngine:
 
     def solve(self, A):
         T, info = solve_block(self.operator(A), self.Bd, self.cfg)
-        _raise_failed(info, T, self.cfg, column_tag=True)
         self.last_info = info
+        try:
+            _raise_failed(info, T, self.cfg, column_tag=True)
+        except Exception as exc:  # the global electrode index, as transfer_matrix reports it
+            if hasattr(exc, "column"):
+                exc.column = self.c0 + exc.column
+            raise
         return T
 
     def solve_rhs(self, A, rhs):

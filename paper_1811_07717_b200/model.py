@@ -118,6 +118,33 @@ class TetMesh:
         return f"TetMesh({self.n_nodes} nodes, {self.n_elements} elements)"
 
 
+class MeshArrays:
+    """A mesh handed over as raw host arrays — nodes (n,3) f64, tetra (m,4),
+    sigma — with no validation and nothing cached across objects: the input of
+    an end-to-end build from host buffers.  Its boundary faces come from the
+    device (hf_boundary_faces, bit-exact with meshgen.py:114-130) the first
+    time they are asked for."""
+
+    def __init__(self, nodes, tetra, sigma, labels=None):
+        self.nodes = np.asarray(nodes, dtype=float)
+        self.tetra = np.asarray(tetra)
+        self.sigma = np.asarray(sigma, dtype=float)
+        self.labels = labels
+        self._boundary = None
+
+    n_nodes = property(lambda self: len(self.nodes))
+    n_elements = property(lambda self: len(self.tetra))
+
+    def boundary_triangles(self):
+        if self._boundary is None:
+            from .topology import boundary_triangles_device
+
+            self._boundary = boundary_triangles_device(self)
+        return self._boundary
+
+    boundary_nodes = TetMesh.boundary_nodes
+
+
 def triangle_areas(nodes, triangles):
     p = nodes[triangles]
     return 0.5 * np.linalg.norm(np.cross(p[:, 1] - p[:, 0], p[:, 2] - p[:, 0]), axis=1)

@@ -6,13 +6,12 @@ Public names and behaviour follow the reference:
   pcg_solve        solver.py:64-111
   transfer_matrix  solver.py:114-141
 The columns of a transfer matrix are solved together by hf_pcg_multi (one
-CSR SpMM per iteration for up to 128 right-hand sides) while each column
+SpMM per iteration for up to 64 right-hand sides) while each column
 keeps its own recurrence, so results do not depend on `threads` or on which
 columns share a batch.
 """
 from __future__ import annotations
 
-import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -23,7 +22,7 @@ from . import _native as N
 from .device import DeviceCsr, PcgOperator, device, ldp_device, width_for
 from .errors import ConvergenceError, ParameterError, SingularPreconditionerError
 
-MAX_BATCH = int(os.environ.get("HFB200_MAX_BATCH", "64"))  # RHS columns per multi-RHS solve
+MAX_BATCH = 64  # RHS columns per multi-RHS solve (the widest kernel instantiation)
 
 
 @dataclass(frozen=True)
@@ -156,6 +155,7 @@ def _raise_failed(info, X, cfg, column_tag):
         f"PCG did not reach {cfg.tolerance:g} in {info.max_iter} iterations "
         f"(best residual {best:.3e})",
         best_x=X[:, j].cpu().numpy(), residual=best, iterations=info.max_iter)
+    exc.local_column = j  # index within this call's block (ordering across ranks)
     if column_tag:
         exc.column = j
     raise exc
