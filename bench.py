@@ -136,11 +136,15 @@ def kernel_roofline(engine, A, rounds=24, config="c2"):
     Bb[:, :k] = engine.Bd[:, :k]
     X = torch.empty_like(Bb)
     ws = torch.empty(N.lib.hf_pcg_workspace_bytes(n, kp, op.Ac.nnz), dtype=torch.uint8, device=Bb.device)
-    ms = (N.C.c_float * 3)()
     flags = N.C.c_int32(0)
-    N.check("hf_pcg_profile", N.lib.hf_pcg_profile(
-        N.C.byref(op.Ac.struct), N.ptr(op.d), N.ptr(Bb), n, kp, rounds, N.ptr(X), ms,
-        N.C.byref(flags), N.ptr(ws), ws.numel(), N.stream_handle()))
+    reps = []
+    for _ in range(3):  # three profiles of `rounds` rounds each: the median per kernel
+        ms3 = (N.C.c_float * 3)()
+        N.check("hf_pcg_profile", N.lib.hf_pcg_profile(
+            N.C.byref(op.Ac.struct), N.ptr(op.d), N.ptr(Bb), n, kp, rounds, N.ptr(X), ms3,
+            N.C.byref(flags), N.ptr(ws), ws.numel(), N.stream_handle()))
+        reps.append([float(v) for v in ms3])
+    ms = np.median(np.array(reps), axis=0)
     nnz = op.Ac.nnz
     xd = max(1, flags.value >> 8)
     # SURVEY.md §8d per launch: the SpMM reads p and the CSR (8 B value + 4 B index
@@ -367,6 +371,15 @@ def run_ours(args):
     info = engine.last_info
     value = L * args.steps / (ms * 1e-3)
 
+    # per-kernel roofline right after the timed region (same GPU state), clocks sampled
+    roof = None
+    A = None
+    if rank == 0:
+        A = engine.assemble()
+        with ClockSampler(local) as rclk:
+            roof = kernel_roofline(engine, A, config=args.config)
+        roof["clocks"] = rclk.summary()
+
     # end to end from host buffers, two ways; the headline `e2e` is the drop-in
     e2e_engine = None if args.no_e2e else e2e_from_arrays(args, prob, cfg, blocks, rank, world, dev, L)
     e2e = None
@@ -375,11 +388,6 @@ def run_ours(args):
     if e2e is None:
         e2e = e2e_engine
 
-    roof = None
-    A = None
-    if rank == 0:
-        A = engine.assemble()
-        roof = kernel_roofline(engine, A, config=args.config)
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         Ah = A.to_scipy()

@@ -33,6 +33,8 @@
  *   hf_grid_tets           meshgen.py:205-223  generate_mesh's Kuhn grid + element centroids
  *   hf_mesh_compact        meshgen.py:224-235  keep labelled elements, np.unique node renumbering
  *   hf_apply_priorities    meshgen.py:247-269  _apply_priorities
+ *   hf_meg_rhs             (none: SPEC.md:8)   MEG transfer right-hand sides S' (C3, parity unpinned)
+ *   hf_meg_primary         (none: SPEC.md:8)   MEG primary-field lead field (C3, parity unpinned)
  *
  * See INTEGRATION.md for the ctypes binding the reference would use.
  */
@@ -208,11 +210,16 @@ int hf_dense_lf(const double* Qc, int32_t ncols, int32_t K, const double* W, int
  * (leadfield.py:179-207).
  *   dof_elems device (sum of DOF sizes) int32, dof_ptr device n_dofs+1 int32
  *   T device n x ldt (L used), U device n x ldu (P used)
- *   Q device P x n_dofs x L row-major */
+ *   Q device P x n_dofs x L row-major
+ *   ws device workspace of hf_eit_sens_workspace_bytes(dof_ptr[n_dofs] - dof_ptr[0])
+ *      bytes (the DOF elements' unit blocks)
+ * The contraction runs on the fp64 tensor pipe (DMMA m8n8k4), one GEMM with
+ * K = 4 |E_m| per DOF. */
+size_t hf_eit_sens_workspace_bytes(int64_t n_dof_elems);
 int hf_eit_sens(const double* nodes, const int32_t* tetra, const int32_t* dof_elems,
                 const int32_t* dof_ptr, int32_t n_dofs, int32_t ground, const double* T,
                 int32_t ldt, int32_t L, const double* U, int32_t ldu, int32_t P, double* Q,
-                void* stream);
+                void* ws, size_t ws_bytes, void* stream);
 
 /* ---------------------------------------------------------------- topology (next rows, §8f) */
 
@@ -291,6 +298,22 @@ int hf_mesh_compact(const int32_t* tetra_all, const int32_t* cent_label, int32_t
  * node labels (device n) and the compartment priorities (device n_comp). */
 int hf_apply_priorities(const int32_t* tetra, int32_t m, const int32_t* node_label,
                         const int32_t* priority, int32_t* labels, void* stream);
+
+/* ---------------------------------------------------------------- MEG (C3)
+ * No reference counterpart (the reference excludes MEG): the FEM
+ * reciprocity formulation on the EEG path's system (csrc/meg.cu header).
+ * coils device n_coils x 8 f64 {rx, ry, rz, nx, ny, nz, weight, 0};
+ * coil_ptr device ncols+1 int32 (sensor s = coils coil_ptr[s]..coil_ptr[s+1]-1). */
+size_t hf_meg_workspace_bytes(int32_t n, int32_t m);
+/* S' (device n x ldb row-major, ncols <= 512 used): the secondary-current flux
+ * operator of every sensor, row `ground` zeroed.  sigma device m f64 (scalar). */
+int hf_meg_rhs(const double* nodes, const int32_t* tetra, const double* sigma, int32_t n, int32_t m,
+               int32_t ground, const double* coils, const int32_t* coil_ptr, int32_t ncols,
+               double* Bt, int32_t ldb, void* ws, size_t ws_bytes, void* stream);
+/* Lp device ncols x 3*n_sources: primary flux of unit x/y/z dipoles at positions
+ * (device n_sources x 3). */
+int hf_meg_primary(const double* coils, const int32_t* coil_ptr, int32_t ncols,
+                   const double* positions, int32_t n_sources, double* Lp, void* stream);
 
 #ifdef __cplusplus
 }

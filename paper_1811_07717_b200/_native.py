@@ -58,7 +58,8 @@ def _load():
         "hf_response_matrix": (C.c_int, [pcsr, P, I32, I32, I32, I32, P, P, P]),
         "hf_lf_tail": (C.c_int, [P, I32, I32, pcsr, P, I32, I32, P, P]),
         "hf_dense_lf": (C.c_int, [P, I32, I32, P, I32, I32, P, I32, P]),
-        "hf_eit_sens": (C.c_int, [P, P, P, P, I32, I32, P, I32, I32, P, I32, I32, P, P]),
+        "hf_eit_sens_workspace_bytes": (SZ, [I64]),
+        "hf_eit_sens": (C.c_int, [P, P, P, P, I32, I32, P, I32, I32, P, I32, I32, P, P, SZ, P]),
         "hf_topology_workspace_bytes": (SZ, [I32, I32, I32]),
         "hf_boundary_faces": (C.c_int, [P, I32, I32, P, C.POINTER(I64), P, SZ, P]),
         "hf_whitney_gt": (C.c_int, [P, P, I32, I32, P, I32, P, P, P, P, C.POINTER(I64), P, SZ, P]),
@@ -69,6 +70,9 @@ def _load():
         "hf_mesh_compact": (C.c_int, [P, P, I32, P, P, P, I32, I32, I32, P, P, P, C.POINTER(I64),
                                       C.POINTER(I64), P, SZ, P]),
         "hf_apply_priorities": (C.c_int, [P, I32, P, P, P, P]),
+        "hf_meg_workspace_bytes": (SZ, [I32, I32]),
+        "hf_meg_rhs": (C.c_int, [P, P, P, I32, I32, I32, P, P, I32, P, I32, P, SZ, P]),
+        "hf_meg_primary": (C.c_int, [P, P, I32, P, I32, P, P]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -85,10 +89,11 @@ EXPORTED = ("hf_version", "hf_last_error", "hf_device_sm_count", "hf_launch_coun
             "hf_csr_prune_workspace_bytes", "hf_csr_prune_count", "hf_csr_prune_fill",
             "hf_pcg_workspace_bytes", "hf_pcg_multi", "hf_pcg_profile", "hf_p1_blocks",
             "hf_p1_assemble_workspace_bytes", "hf_p1_assemble_prepare", "hf_p1_assemble_fill",
-            "hf_response_matrix", "hf_lf_tail", "hf_dense_lf", "hf_eit_sens",
+            "hf_response_matrix", "hf_lf_tail", "hf_dense_lf", "hf_eit_sens_workspace_bytes", "hf_eit_sens",
             "hf_topology_workspace_bytes", "hf_boundary_faces", "hf_whitney_gt",
             "hf_nearest_center", "hf_locate", "hf_grid_tets", "hf_mesh_compact_workspace_bytes",
-            "hf_mesh_compact", "hf_apply_priorities")
+            "hf_mesh_compact", "hf_apply_priorities", "hf_meg_workspace_bytes", "hf_meg_rhs",
+            "hf_meg_primary")
 
 
 class NativeError(RuntimeError):

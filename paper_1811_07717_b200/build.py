@@ -15,7 +15,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIBDIR = os.path.join(HERE, "_lib")
 LIB = os.path.join(LIBDIR, "libhfb200.so")
-SOURCES = ["abi.cu", "pcg.cu", "assemble.cu", "tail.cu", "topology.cu", "dofmap.cu", "meshgen.cu"]
+SOURCES = ["abi.cu", "pcg.cu", "assemble.cu", "tail.cu", "topology.cu", "dofmap.cu", "meshgen.cu", "meg.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -147,18 +147,36 @@ __device__ void unit_block(const double* __restrict__ nodes, const int32_t* __re
 // chunk's U and T rows into shared memory, forms S, and every warp accumulates
 // its 8x8 output tiles with DMMA.  Shared rows are padded to a stride = 4 mod 16
 // doubles so the A/B fragment loads are bank-conflict free.
-constexpr int ES_EC = 16;             // elements per chunk -> K = 64 per chunk
+constexpr int ES_EC = 16;             // elements per chunk -> K = 64 per chunk (one corner per 4 threads)
 constexpr int ES_K = 4 * ES_EC;
-constexpr int ES_MAXP = 64, ES_MAXL = 64;
+constexpr int ES_MAXP = 32, ES_MAXL = 64;  // patterns x electrode columns per CTA
 constexpr int ES_WARPS = ES_THREADS / 32;
 constexpr int ES_MAXT = (ES_MAXP / 8) * (ES_MAXL / 8) / ES_WARPS;  // output tiles per warp
 
 __host__ __device__ inline int es_stride(int w) { return ((w + 7) / 8) * 8 + ((((w + 7) / 8) * 8) % 16 == 0 ? 4 : 12); }
 
-__global__ void __launch_bounds__(ES_THREADS, 2)
-    k_eit_sens(const double* __restrict__ nodes, const int32_t* __restrict__ tetra,
+// Unit-sigma blocks of every DOF element, in dof_elems order (one thread each):
+// the divisions of unit_block run massively parallel here instead of on 16
+// threads of a sensitivity CTA.  Kbuf: (sum of DOF sizes) x 16.
+__global__ void k_dof_blocks(const double* __restrict__ nodes, const int32_t* __restrict__ tetra,
+                             const int32_t* __restrict__ dof_elems, int n_elems, int ground,
+                             double* __restrict__ Kbuf) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n_elems) return;
+  int32_t conn[4];
+  const int e = dof_elems[i];
+#pragma unroll
+  for (int a = 0; a < 4; ++a) conn[a] = tetra[4 * (size_t)e + a];
+  double K[16];
+  unit_block(nodes, conn, ground, K);
+#pragma unroll
+  for (int q = 0; q < 16; ++q) Kbuf[(size_t)i * 16 + q] = K[q];
+}
+
+__global__ void __launch_bounds__(ES_THREADS, 3)
+    k_eit_sens(const double* __restrict__ Kbuf, const int32_t* __restrict__ tetra,
                const int32_t* __restrict__ dof_elems, const int32_t* __restrict__ dof_ptr,
-               int n_dofs, int ground, const double* __restrict__ T, int ldt, int L,
+               int n_dofs, const double* __restrict__ T, int ldt, int L,
                const double* __restrict__ U, int ldu, int P, double* __restrict__ Q) {
   extern __shared__ double sh[];
   const int m = blockIdx.x;
@@ -167,68 +185,84 @@ __global__ void __launch_bounds__(ES_THREADS, 2)
   const int SP = es_stride(np_), SL = es_stride(nl);
   double* sS = sh;                      // [ES_K][SP]
   double* sT = sS + ES_K * SP;          // [ES_K][SL]
-  double* sU = sT + ES_K * SL;          // [ES_K][np_]
-  double* sK = sU + ES_K * np_;         // [ES_EC][16]
-  __shared__ int32_t sC[ES_EC][4];
+  double* sU = sT + ES_K * SL;          // [ES_K][SP]
+  double* sK = sU + ES_K * SP;          // [ES_EC][16]
+  __shared__ int32_t sC[2][ES_K];       // corner nodes of this chunk and the next
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
   const int MT = (np_ + 7) / 8, NTt = (nl + 7) / 8, ntile = MT * NTt;
+  // gather layout: 4 threads per chunk corner k = tid / 4; thread gq of a corner owns
+  // columns gq, gq + 4, ... so a warp's accesses are 8 corners x 4 consecutive
+  // doubles: one sector per corner in global memory, conflict-free in shared memory
+  const int gk = tid >> 2, gq = tid & 3;
   double acc[ES_MAXT][2];
 #pragma unroll
   for (int j = 0; j < ES_MAXT; ++j) acc[j][0] = acc[j][1] = 0.0;
   const int e0 = dof_ptr[m], e1 = dof_ptr[m + 1];
-  for (int eb = e0; eb < e1; eb += ES_EC) {
+  auto load_conn = [&](int eb, int buf) {
+    if (tid < ES_K) {
+      const int e = eb + tid / 4;
+      sC[buf][tid] = e < e1 ? tetra[4 * (size_t)dof_elems[e] + (tid & 3)] : -1;
+    }
+  };
+  load_conn(e0, 0);
+  // padded operand rows/columns (p >= np_, l >= nl) stay zero for the whole CTA
+  for (int o = tid; o < ES_K * SP; o += ES_THREADS) sS[o] = 0.0;
+  for (int o = tid; o < ES_K * SL; o += ES_THREADS) sT[o] = 0.0;
+  __syncthreads();
+  int buf = 0;
+  for (int eb = e0; eb < e1; eb += ES_EC, buf ^= 1) {
     const int ne = min(ES_EC, e1 - eb);
-    if (tid < ES_EC * 4) {
-      const int e = tid / 4;
-      sC[e][tid % 4] = e < ne ? tetra[4 * (size_t)dof_elems[eb + e] + (tid % 4)] : -1;
-    }
+    // 1) this thread's T and U row segments into registers: every load in flight at once
+    const int node = sC[buf][gk];
+    double tv[ES_MAXL / 4], uv[ES_MAXP / 4];
+#pragma unroll
+    for (int i = 0; i < ES_MAXL / 4; ++i)
+      tv[i] = (node >= 0 && gq + 4 * i < nl) ? __ldg(T + (size_t)node * ldt + l0 + gq + 4 * i) : 0.0;
+#pragma unroll
+    for (int i = 0; i < ES_MAXP / 4; ++i)
+      uv[i] = (node >= 0 && gq + 4 * i < np_) ? __ldg(U + (size_t)node * ldu + p0 + gq + 4 * i) : 0.0;
+    // 2) the chunk's element blocks (k_dof_blocks), one entry per thread
+    const double kv = tid < 16 * ne ? __ldg(Kbuf + (size_t)(eb - dof_ptr[0]) * 16 + tid) : 0.0;
+    // 3) next chunk's corners
+    load_conn(eb + ES_EC, buf ^ 1);
+#pragma unroll
+    for (int i = 0; i < ES_MAXL / 4; ++i)
+      if (gq + 4 * i < nl) sT[gk * SL + gq + 4 * i] = tv[i];
+#pragma unroll
+    for (int i = 0; i < ES_MAXP / 4; ++i)
+      if (gq + 4 * i < np_) sU[gk * SP + gq + 4 * i] = uv[i];
+    sK[tid] = kv;
     __syncthreads();
-    if (tid < ne) unit_block(nodes, sC[tid], ground, sK + 16 * tid);
-    for (int o = tid; o < ES_K * np_; o += ES_THREADS) {  // U rows of the chunk's corners
-      const int k = o / np_, p = o % np_;
-      const int node = sC[k / 4][k % 4];
-      sU[o] = node >= 0 ? __ldg(U + (size_t)node * ldu + p0 + p) : 0.0;
-    }
-    for (int o = tid; o < ES_K * nl; o += ES_THREADS) {  // T rows of the chunk's corners
-      const int k = o / nl, l = o % nl;
-      const int node = sC[k / 4][k % 4];
-      sT[k * SL + l] = node >= 0 ? __ldg(T + (size_t)node * ldt + l0 + l) : 0.0;
-    }
-    __syncthreads();
-    for (int o = tid; o < ES_K * np_; o += ES_THREADS) {  // S = K_e u_e
-      const int k = o / np_, p = o % np_, e = k / 4, i = k % 4;
-      double v = 0.0;
+    // 4) S[k, p] = K_e[i, :] u_e[:, p]
+    {
+      const int e = gk / 4, i = gk & 3;
       if (e < ne) {
         const double* K = sK + 16 * e + 4 * i;
-        const double* u = sU + (size_t)(4 * e) * np_ + p;
-        v = K[0] * u[0];
-        v = fma(K[1], u[np_], v);
-        v = fma(K[2], u[2 * np_], v);
-        v = fma(K[3], u[3 * np_], v);
+        const double* u = sU + (size_t)(4 * e) * SP;
+        for (int pp = gq; pp < np_; pp += 4) {
+          double v = K[0] * u[pp];
+          v = fma(K[1], u[SP + pp], v);
+          v = fma(K[2], u[2 * SP + pp], v);
+          v = fma(K[3], u[3 * SP + pp], v);
+          sS[gk * SP + pp] = v;
+        }
+      } else {
+        for (int pp = gq; pp < np_; pp += 4) sS[gk * SP + pp] = 0.0;
       }
-      sS[k * SP + p] = v;
-    }
-    // zero the padded output rows/columns' operands (p >= np_, l >= nl) once per chunk
-    for (int o = tid; o < ES_K * (MT * 8 - np_); o += ES_THREADS) {
-      const int w = MT * 8 - np_;
-      sS[(o / w) * SP + np_ + o % w] = 0.0;
-    }
-    for (int o = tid; o < ES_K * (NTt * 8 - nl); o += ES_THREADS) {
-      const int w = NTt * 8 - nl;
-      sT[(o / w) * SL + nl + o % w] = 0.0;
     }
     __syncthreads();
+    // 5) Q tiles += S' Tg on the fp64 tensor pipe; the warp's tiles advance together
+    //    through k so their DMMA chains overlap
+#pragma unroll 2
+    for (int k0 = 0; k0 < ES_K; k0 += 4) {
+      const double* ar = sS + (size_t)(k0 + t4) * SP + g;  // A[row p][k] = S[k][p]
+      const double* br = sT + (size_t)(k0 + t4) * SL + g;  // B[k][col l] = Tg[k][l]
 #pragma unroll
-    for (int j = 0; j < ES_MAXT; ++j) {
-      const int ti = warp + ES_WARPS * j;
-      if (ti >= ntile) break;
-      const int mt = ti % MT, nt = ti / MT;
-      const double* ap = sS + (size_t)t4 * SP + mt * 8 + g;  // A[row p][k] = S[k][p]
-      const double* bp = sT + (size_t)t4 * SL + nt * 8 + g;  // B[k][col l] = Tg[k][l]
-#pragma unroll 4
-      for (int k0 = 0; k0 < ES_K; k0 += 4)
-        dmma_8x8x4(acc[j][0], acc[j][1], ap[(size_t)k0 * SP], bp[(size_t)k0 * SL]);
+      for (int j = 0; j < ES_MAXT; ++j) {
+        const int ti = warp + ES_WARPS * j;
+        if (ti < ntile) dmma_8x8x4(acc[j][0], acc[j][1], ar[(ti % MT) * 8], br[(ti / MT) * 8]);
+      }
     }
     __syncthreads();
   }
@@ -317,25 +351,45 @@ extern "C" int hf_dense_lf(const double* Qc, int32_t ncols, int32_t K, const dou
                    reinterpret_cast<cudaStream_t>(stream));
 }
 
+extern "C" size_t hf_eit_sens_workspace_bytes(int64_t n_dof_elems) {
+  return (size_t)(n_dof_elems + 1) * 16 * sizeof(double) + 256;
+}
+
 extern "C" int hf_eit_sens(const double* nodes, const int32_t* tetra, const int32_t* dof_elems,
                            const int32_t* dof_ptr, int32_t n_dofs, int32_t ground, const double* T,
                            int32_t ldt, int32_t L, const double* U, int32_t ldu, int32_t P,
-                           double* Q, void* stream) {
-  if (!nodes || !tetra || !dof_elems || !dof_ptr || !T || !U || !Q || L <= 0 || P <= 0 ||
-      ldt < L || ldu < P) {
+                           double* Q, void* ws, size_t ws_bytes, void* stream) {
+  if (!nodes || !tetra || !dof_elems || !dof_ptr || !T || !U || !Q || !ws || L <= 0 || P <= 0 ||
+      ldt < L || ldu < P || n_dofs < 0) {
     set_error("hf_eit_sens: bad argument");
     return HF_ERR_ARG;
   }
   if (n_dofs == 0) return HF_OK;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  int32_t ends[2] = {0, 0};
+  HF_CUDA(cudaMemcpyAsync(&ends[0], dof_ptr, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  HF_CUDA(cudaMemcpyAsync(&ends[1], dof_ptr + n_dofs, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  HF_CUDA(cudaStreamSynchronize(s));
+  const int64_t ne = (int64_t)ends[1] - ends[0];
+  if (ws_bytes < hf_eit_sens_workspace_bytes(ne)) {
+    set_error("hf_eit_sens: workspace too small");
+    return HF_ERR_WORKSPACE;
+  }
+  double* Kbuf = reinterpret_cast<double*>(ws);
+  if (ne > 0) {
+    tail::k_dof_blocks<<<(int)((ne + 255) / 256), 256, 0, s>>>(nodes, tetra, dof_elems + ends[0], (int)ne,
+                                                               ground, Kbuf);
+    HF_LAUNCH_CHECK();
+    count_launches(1);
+  }
   const int nl = std::min(L, tail::ES_MAXL), np_ = std::min(P, tail::ES_MAXP);
-  const size_t smem = sizeof(double) * ((size_t)tail::ES_K * (tail::es_stride(np_) + tail::es_stride(nl) + np_) +
+  const size_t smem = sizeof(double) * ((size_t)tail::ES_K * (2 * tail::es_stride(np_) + tail::es_stride(nl)) +
                                         16 * tail::ES_EC);
   HF_CUDA(cudaFuncSetAttribute(tail::k_eit_sens, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                (int)smem));
   dim3 grid(n_dofs, (L + tail::ES_MAXL - 1) / tail::ES_MAXL, (P + tail::ES_MAXP - 1) / tail::ES_MAXP);
-  tail::k_eit_sens<<<grid, tail::ES_THREADS, smem, s>>>(nodes, tetra, dof_elems, dof_ptr, n_dofs,
-                                                        ground, T, ldt, L, U, ldu, P, Q);
+  tail::k_eit_sens<<<grid, tail::ES_THREADS, smem, s>>>(Kbuf, tetra, dof_elems, dof_ptr, n_dofs, T,
+                                                        ldt, L, U, ldu, P, Q);
   HF_LAUNCH_CHECK();
   count_launches(1);
   return HF_OK;

@@ -289,9 +289,10 @@ def dof_sensitivities_device(mesh, dofs, ground, T, U, L, P):
     dp = torch.from_numpy(ptr.astype(np.int32)).to(dev)
     nd = dofs.n_dofs
     Q = torch.empty((P, nd, L), dtype=torch.float64, device=dev)
+    ws = torch.empty(N.lib.hf_eit_sens_workspace_bytes(len(elems)), dtype=torch.uint8, device=dev)
     N.check("hf_eit_sens", N.lib.hf_eit_sens(
         N.ptr(dm.nodes), N.ptr(dm.tetra), N.ptr(de), N.ptr(dp), nd, int(ground), N.ptr(T),
-        T.stride(0), L, N.ptr(U), U.stride(0), P, N.ptr(Q), N.stream_handle()))
+        T.stride(0), L, N.ptr(U), U.stride(0), P, N.ptr(Q), N.ptr(ws), ws.numel(), N.stream_handle()))
     return Q
 
 

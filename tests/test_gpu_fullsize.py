@@ -154,8 +154,13 @@ def test_c5_columns_match_reference(cuda):
     assert mesh.n_nodes == int(gd["n_nodes"])
     assert sha(np.asarray(mesh.nodes)) == str(gd["nodes_sha"])
     assert sha(np.asarray(mesh.tetra, dtype=np.int64)) == str(gd["tetra_sha"])
-    A, g = assemble_A_device(mesh, prob.electrodes)
+    el = prob.electrodes
+    np.testing.assert_array_equal(np.cumsum([0] + [len(t) for t in el.triangle_ids]), gd["tri_ptr"])
+    assert sha(np.concatenate(el.triangle_ids).astype(np.int64)) == str(gd["tri_ids_sha"])
+    A, g = assemble_A_device(mesh, el)
     assert A.nnz == int(gd["A_nnz"]) and int(g) == int(gd["ground"])
+    assert sha(A.indptr.cpu().numpy()) == str(gd["A_sha_indptr"])
+    assert sha(A.indices.cpu().numpy()) == str(gd["A_sha_indices"])
     cols = [int(c) for c in gd["columns"]]
     T, info = transfer_device(A, prob.B.tocsc()[:, cols], PcgConfig(tolerance=TOL))
     d_it = np.abs(info.iterations.astype(np.int64) - gd["iters"])

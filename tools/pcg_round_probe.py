@@ -24,6 +24,11 @@ def main():
     prob = synthetic.eeg_problem(a.config, device=True)
     eng = EegEngine(prob.mesh, prob.electrodes, prob.G, B=prob.B, C=prob.C, R=prob.R)
     op = PcgOperator(eng.assemble(), "ldp")
+    lens = torch.diff(op.Ac.indptr.long()).cpu().numpy()
+    import numpy as np
+    h = np.bincount(lens)
+    print("SpMM copy row lengths:", {int(k): int(v) for k, v in enumerate(h) if v},
+          "rows > 8:", int((lens > 8).sum()))
     Bb = eng.Bd[:, :a.kp].contiguous()
     X = torch.empty_like(Bb)
     ws = torch.empty(N.lib.hf_pcg_workspace_bytes(op.n, a.kp, op.Ac.nnz), dtype=torch.uint8, device="cuda")
