@@ -119,7 +119,7 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- our arm
-def kernel_roofline(engine, A, rounds=24, config="c2"):
+def kernel_roofline(Bd, A, rounds=24, config="c2"):
     """Per-kernel CUDA-event timing of a PCG round at the bench's batch width,
     algorithmic bytes per launch, fraction of the HBM peak."""
     import torch
@@ -130,10 +130,10 @@ def kernel_roofline(engine, A, rounds=24, config="c2"):
 
     op = PcgOperator(A, "ldp")
     n = op.n
-    kp = width_for(op.batch_width(engine.Bd.shape[1], MAX_BATCH))  # the solver's own batch width
-    Bb = torch.zeros((n, kp), dtype=torch.float64, device=engine.Bd.device)
-    k = min(kp, engine.Bd.shape[1])
-    Bb[:, :k] = engine.Bd[:, :k]
+    kp = width_for(op.batch_width(Bd.shape[1], MAX_BATCH))  # the solver's own batch width
+    Bb = torch.zeros((n, kp), dtype=torch.float64, device=Bd.device)
+    k = min(kp, Bd.shape[1])
+    Bb[:, :k] = Bd[:, :k]
     X = torch.empty_like(Bb)
     ws = torch.empty(N.lib.hf_pcg_workspace_bytes(n, kp, op.Ac.nnz), dtype=torch.uint8, device=Bb.device)
     flags = N.C.c_int32(0)
@@ -185,21 +185,40 @@ def kernel_roofline(engine, A, rounds=24, config="c2"):
                         for k2, d in kern.items()}}
 
 
-def cpu_baseline_port(A, b, iters_per_col, sample_iters=150):
-    """The oracle's numpy PCG (solver.py:64-111 restated) on one host core, for a
-    bounded number of iterations of one C2 column; RHS-solves/s extrapolated."""
-    import oracle
+def cpu_baseline(A, b, iters_per_col, sample_iters=200):
+    """The reference's own pcg_solve (baseline/_ref, unmodified; solver.py:64-111)
+    on one host core for a bounded sample of one C2 column (max_iterations =
+    sample_iters; the ConvergenceError it then raises ends the sample), RHS-solves/s
+    extrapolated to the measured iterations per column.  Falls back to the
+    oracle's restatement (kind "port") only if baseline/_ref is missing."""
     from threadpoolctl import threadpool_limits
 
+    try:
+        _import_reference()
+        from headfem.errors import ConvergenceError
+        from headfem.solver import PcgConfig, pcg_solve
+
+        def run(k):
+            try:
+                pcg_solve(A, b, PcgConfig(tolerance=1e-8, max_iterations=k))
+            except ConvergenceError:
+                pass
+        kind, what = "reference", "headfem.solver.pcg_solve (baseline/_ref)"
+    except Exception:
+        import oracle
+
+        def run(k):
+            oracle.pcg_solve(A, b, oracle.PcgSettings(), iterations_cap=k)
+        kind, what = "port", "the oracle's pcg_solve restatement"
     with threadpool_limits(1):
-        oracle.pcg_solve(A, b, oracle.PcgSettings(), iterations_cap=3)
+        run(3)
         t0 = time.perf_counter()
-        oracle.pcg_solve(A, b, oracle.PcgSettings(), iterations_cap=sample_iters)
+        run(sample_iters)
         dt = time.perf_counter() - t0
     t_iter = dt / sample_iters
-    return {"value": 1.0 / (t_iter * iters_per_col), "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"{sample_iters} PCG iterations of electrode column 0 on the bench system "
-                      f"({t_iter * 1e3:.1f} ms/iteration, 1 thread), extrapolated to "
+    return {"value": 1.0 / (t_iter * iters_per_col), "unit": UNIT, "cores": 1, "kind": kind,
+            "sample": f"{sample_iters} PCG iterations of electrode column 0 on the bench system through "
+                      f"{what} ({t_iter * 1e3:.1f} ms/iteration, 1 thread), extrapolated to "
                       f"{iters_per_col:.0f} iterations per column",
             "ms_per_iteration": round(t_iter * 1e3, 3)}
 
@@ -312,6 +331,68 @@ def e2e_dropin(args, prob, cfg, L):
                    "memory out"}
 
 
+def run_meg(args):
+    """C3 (BASELINE.json configs[2]): the 306-sensor MEG lead field on the C2 mesh
+    (paper_1811_07717_b200.meg; parity unpinned, the reference has no MEG).  One
+    step = assembly -> S' (hf_meg_rhs) -> 306 PCG solves -> primary field + T'G."""
+    import torch
+
+    from paper_1811_07717_b200 import _native as N
+    from paper_1811_07717_b200 import meg, model, synthetic
+    from paper_1811_07717_b200.solver import PcgConfig
+
+    torch.cuda.set_device(0)
+    cfg = PcgConfig(tolerance=1e-8)
+    prob = synthetic.eeg_problem("c2", device=True, with_G=False)
+    sensors = meg.helmet_306()
+    eng = meg.MegEngine(prob.mesh, sensors, prob.sources, cfg)
+    for _ in range(args.warmup):
+        eng.build()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = N.lib.hf_launch_count()
+    with ClockSampler(0) as clocks:
+        e0.record()
+        for _ in range(args.steps):
+            Lf = eng.build()
+        e1.record()
+        torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = N.lib.hf_launch_count() - launches0
+    ns = sensors.n_sensors
+    roof = kernel_roofline(eng.rhs(), eng.assemble(), config="c3")
+    # end to end from host arrays: fresh mesh object, sensors and source ids every step
+    w0 = time.perf_counter()
+    for _ in range(args.steps):
+        mesh = model.MeshArrays(prob.mesh.nodes, prob.mesh.tetra, prob.mesh.sigma)
+        e2 = meg.MegEngine(mesh, sensors, prob.sources, cfg)
+        lf_host = e2.build(to_host=True)
+    wall = (time.perf_counter() - w0) / args.steps
+    h2d = prob.mesh.nodes.nbytes + 4 * prob.mesh.tetra.size + prob.mesh.sigma.nbytes + \
+        sensors.coils.nbytes + 4 * len(sensors.coil_ptr) + 4 * len(prob.sources.element_ids) + \
+        prob.sources.positions.nbytes
+    info = eng.last_info
+    out = {"metric": METRIC, "value": round(ns / (ms * 1e-3), 3), "unit": UNIT, "n_gpus": 1,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 2), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (C2 mesh; Elekta-like 102-site helmet: 102 magnetometers + 204 planar "
+                   "gradiometers; volume-weighted random sources)",
+           "config": {"workload": f"c3: {prob.mesh.n_nodes:,}-node 4-compartment sphere mesh, {ns}-sensor MEG "
+                                  f"lead field, {prob.sources.n_sources:,} dipole sources (parity unpinned: "
+                                  "the reference has no MEG, SPEC.md:8)", "config": "c3",
+                      "n_nodes": int(prob.mesh.n_nodes), "sensors": ns, "sources": int(prob.sources.n_sources),
+                      "lf_shape": list(Lf.shape), "tolerance": cfg.tolerance, "precision": "fp64",
+                      "parallelism": "sensor-columns x1"},
+           "pcg_iterations": {"min": int(info.iterations.min()), "max": int(info.iterations.max()),
+                              "mean": float(np.mean(info.iterations))},
+           "gpu_launches": int(launches), "roofline": roof, "cpu_baseline": None,
+           "e2e": {"value": ns / wall, "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                   "d2h_bytes_per_step": int(lf_host.nbytes), "ms_per_step": round(wall * 1e3, 2),
+                   "api": "MegEngine(MeshArrays(nodes, tetra, sigma), helmet_306(), sources).build(to_host=True)"},
+           "clocks": clocks.summary()}
+    print(json.dumps(out), flush=True)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -377,7 +458,7 @@ def run_ours(args):
     if rank == 0:
         A = engine.assemble()
         with ClockSampler(local) as rclk:
-            roof = kernel_roofline(engine, A, config=args.config)
+            roof = kernel_roofline(engine.Bd, A, config=args.config)
         roof["clocks"] = rclk.summary()
 
     # end to end from host buffers, two ways; the headline `e2e` is the drop-in
@@ -392,7 +473,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         Ah = A.to_scipy()
         b = prob.B[:, 0].toarray().ravel()
-        cpu = cpu_baseline_port(Ah, b, float(np.mean(info.iterations)))
+        cpu = cpu_baseline(Ah, b, float(np.mean(info.iterations)))
     clk = clocks.summary()
     if rank == 0:
         lf_ok = LF is not None and bool(torch.isfinite(LF).all().item())
@@ -497,6 +578,9 @@ def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    if args.config == "c3":
+        print(json.dumps({"impl": "reference", "unavailable": "the reference has no MEG lead field (SPEC.md:8)"}))
+        return
     import multiprocessing as mp
 
     hf = _import_reference()
@@ -553,7 +637,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=["c1", "c2", "c5"], default="c2")
+    ap.add_argument("--config", choices=["c1", "c2", "c3", "c5"], default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-cores", type=int, default=0)
@@ -562,6 +646,8 @@ def main():
         log("note: fewer than 3 warm-up steps")
     if args.impl == "reference":
         run_reference(args)
+    elif args.config == "c3":
+        run_meg(args)
     else:
         run_ours(args)
 

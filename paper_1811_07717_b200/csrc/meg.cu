@@ -1,15 +1,16 @@
 // MEG lead field on the same FEM system (BASELINE.json configs[2], C3).
 //
 // The reference has no MEG: this is the standard FEM reciprocity
-// formulation, parity unpinned.  With u = A^-1 G q the potential of a dipole
-// source (the EEG path's source matrix G, fem.py:391-422), the flux of the
+// formulation, parity unpinned.  With u = -A^-1 G q the potential of a dipole
+// source (the EEG path's source matrix G, fem.py:391-422, whose sign makes the
+// EEG lead field -R M^-1 T'G, leadfield.py:129), the flux of the
 // secondary currents -sigma grad u through coil c (position r_c, normal n_c) is
 //   B_sec,c = sum_j u_j S[c, j],
 //   S[c, j] = -mu0/4pi sum_{e ∋ j} sigma_e V_e grad(phi_j)|_e . ((r_c - x_e) x n_c) / |r_c - x_e|^3
 // (one-point quadrature at the element centroid x_e), so the MEG transfer
 // matrix is T_meg = A^-1 S' — one RHS column per sensor through the same
 // multi-RHS PCG as the electrodes — and the lead field is
-//   L = L_primary + T_meg' G,
+//   L = L_primary - T_meg' G,
 //   L_primary[s, 3k + a] = mu0/4pi sum_{c in s} w_c ((r_c - r_k) x n_c)_a / |r_c - r_k|^3.
 // A sensor is a weighted set of point coils (magnetometer: one coil; planar
 // gradiometer: two coils, weights +-1/baseline).

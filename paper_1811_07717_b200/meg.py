@@ -8,7 +8,10 @@ and the same gather + DMMA tail as the EEG lead field:
 
     S'     = hf_meg_rhs(mesh, sensors)           n x n_sensors
     T_meg  = A^-1 S'                              hf_pcg_multi (solver.solve_block)
-    L      = L_primary + T_meg' G                 hf_meg_primary + hf_lf_tail (W = I)
+    L      = L_primary - T_meg' G                 hf_meg_primary + hf_lf_tail (W = -I)
+
+The minus sign: the reference's source matrix enters with the potential
+u = -A^-1 G q (its EEG lead field is L = -R M^-1 T'G, leadfield.py:129).
 
 A is assembled without electrode contact terms and grounded at the lowest
 boundary node (the reference's ground_node rule with no electrodes,
@@ -24,7 +27,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .device import DeviceCsr, device
+from .device import device
 from .fem import DeviceMesh, assemble_device, blocks_device
 from .leadfield import LeadField, lf_tail_device
 from .solver import PcgConfig, _raise_failed, solve_block
@@ -90,7 +93,7 @@ class MegEngine:
         self.cfg = cfg
         self.mesh = mesh
         self.dmesh = DeviceMesh.of(mesh)
-        self.sigma = torch.from_numpy(np.ascontiguousarray(mesh.sigma, dtype=np.float64)).to(dev)
+        self.sigma = torch.from_numpy(np.array(mesh.sigma, dtype=np.float64)).to(dev)
         if self.sigma.dim() != 1:
             raise ValueError("the MEG right-hand side needs scalar conductivities")
         self.ground = _ground(mesh)
@@ -133,7 +136,7 @@ class MegEngine:
         _raise_failed(info, T, self.cfg, column_tag=True)
         self.last_info = info
         ns = self.sensors.n_sensors
-        L = self.primary() + lf_tail_device(T, self.Gt, np.eye(ns))
+        L = self.primary() + lf_tail_device(T, self.Gt, -np.eye(ns))  # u = -A^-1 G q
         return L.cpu().numpy() if to_host else L
 
 
