@@ -29,6 +29,9 @@
  *   hf_boundary_faces      meshgen.py:101-134  TetMesh.boundary_triangles
  *   hf_whitney_gt          fem.py:291-422      assemble_G (Whitney source matrix), as G'
  *   hf_nearest_center      leadfield.py:96-99  build_dof_map: owner = argmin ||c_i - centre_j||
+ *                          fem.py:157-173      ElectrodeSet.from_centers (nearest centre + distance)
+ *   hf_triangle_centroids  fem.py:163          boundary-triangle centroids of from_centers
+ *   hf_ground_node         fem.py:188-194      ground_node
  *   hf_locate              geometry.py:147-374 Segmentation.locate (ray-parity point location)
  *   hf_grid_tets           meshgen.py:205-223  generate_mesh's Kuhn grid + element centroids
  *   hf_mesh_compact        meshgen.py:224-235  keep labelled elements, np.unique node renumbering
@@ -249,7 +252,22 @@ int hf_whitney_gt(const double* nodes, const int32_t* tetra, int32_t n, int32_t 
  * (build_dof_map, leadfield.py:96-99).  points (n_points x 3), centers
  * (n_centers x 3) row-major fp64, owner int32; all device.  No workspace. */
 int hf_nearest_center(const double* points, int32_t n_points, const double* centers,
-                      int32_t n_centers, int32_t* owner, void* stream);
+                      int32_t n_centers, int32_t* owner, double* dist, void* stream);
+/* dist (device n_points f64, or NULL): the winning distance, as np.linalg.norm
+ * computes it — ElectrodeSet.from_centers' coverage test d <= radius
+ * (fem.py:164-167) uses the same routine on boundary-triangle centroids. */
+
+/* Centroids ((a + b) + c) / 3 of n_tri triangles (device n_tri x 3 int32 node ids),
+ * numpy's mean over 3 rows (fem.py:163).  cent device n_tri x 3 f64. */
+int hf_triangle_centroids(const double* nodes, const int32_t* tri, int32_t n_tri, double* cent,
+                          void* stream);
+
+/* ground_node (fem.py:188-194): the lowest boundary node (nodes of bfaces, device
+ * n_bfaces x 3 int32) not covered by an electrode triangle (etri, device n_etri x 3
+ * int32); *ground (host) = -1 if there is none.  ws: hf_ground_node_workspace_bytes(n). */
+size_t hf_ground_node_workspace_bytes(int32_t n);
+int hf_ground_node(const int32_t* bfaces, int32_t n_bfaces, const int32_t* etri, int32_t n_etri,
+                   int32_t n, void* ws, int32_t* ground, void* stream);
 
 /* ---------------------------------------------------------------- mesh generation (next row #4, §8f) */
 

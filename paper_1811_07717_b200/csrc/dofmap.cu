@@ -23,7 +23,8 @@ constexpr int NC_TILE = 2048;  // centres per shared-memory tile (48 KB)
 
 __global__ void __launch_bounds__(NC_T) k_nearest(const double* __restrict__ pts, int E,
                                                  const double* __restrict__ ctr, int m,
-                                                 int32_t* __restrict__ owner) {
+                                                 int32_t* __restrict__ owner,
+                                                 double* __restrict__ dist) {
   __shared__ double cx[NC_TILE], cy[NC_TILE], cz[NC_TILE];
   double px[NC_PPT], py[NC_PPT], pz[NC_PPT], bs[NC_PPT], br[NC_PPT];
   int bi[NC_PPT];
@@ -70,7 +71,10 @@ __global__ void __launch_bounds__(NC_T) k_nearest(const double* __restrict__ pts
 #pragma unroll
   for (int u = 0; u < NC_PPT; ++u) {
     const size_t i = base + (size_t)u * NC_T;
-    if (i < (size_t)E) owner[i] = bi[u];
+    if (i < (size_t)E) {
+      owner[i] = bi[u];
+      if (dist != nullptr) dist[i] = br[u];
+    }
   }
 }
 
@@ -80,7 +84,7 @@ __global__ void __launch_bounds__(NC_T) k_nearest(const double* __restrict__ pts
 using namespace hf;
 
 extern "C" int hf_nearest_center(const double* points, int32_t n_points, const double* centers,
-                                 int32_t n_centers, int32_t* owner, void* stream) {
+                                 int32_t n_centers, int32_t* owner, double* dist, void* stream) {
   if (n_points < 0 || n_centers <= 0 || !centers || (n_points > 0 && (!points || !owner))) {
     set_error("hf_nearest_center: bad argument");
     return HF_ERR_ARG;
@@ -89,7 +93,7 @@ extern "C" int hf_nearest_center(const double* points, int32_t n_points, const d
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const int per = dof::NC_T * dof::NC_PPT;
   const int nb = (n_points + per - 1) / per;
-  dof::k_nearest<<<nb, dof::NC_T, 0, s>>>(points, n_points, centers, n_centers, owner);
+  dof::k_nearest<<<nb, dof::NC_T, 0, s>>>(points, n_points, centers, n_centers, owner, dist);
   HF_LAUNCH_CHECK();
   count_launches(1);
   return HF_OK;

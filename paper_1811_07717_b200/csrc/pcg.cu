@@ -364,6 +364,9 @@ __global__ void __launch_bounds__(Map<KP>::NT)
 constexpr int ELL_LONG = 1 << 30;
 constexpr int ELL_OPT = 5;  // first slot gathered only when it holds an entry
 constexpr int ELL_HB = 4;   // gathers in flight per batch
+#ifndef HF_SLOT_SHFL
+#define HF_SLOT_SHFL 0
+#endif
 
 __global__ void k_ell_fill(int n, const int32_t* __restrict__ indptr,
                            const int32_t* __restrict__ indices, const double* __restrict__ val,
@@ -472,6 +475,18 @@ __global__ void __launch_bounds__(Map<KP>::NT, 2)
     int ciN[SPL];
     double cvN[SPL];
     load_slots(rowN, ciN, cvN);  // next tile's slots in flight during this one
+#if HF_SLOT_SHFL
+    int cc[ELL_W];
+    double vs[ELL_W];
+#pragma unroll
+    for (int e = 0; e < ELL_W; ++e) {  // slot e sits in lane e % LPR, register e / LPR
+      cc[e] = __shfl_sync(FULL, ci[e / LPR], e % LPR, LPR);
+      vs[e] = __shfl_sync(FULL, cv[e / LPR], e % LPR, LPR);
+    }
+    const int c0x = cc[0];
+    cc[0] &= ELL_LONG - 1;
+    if (row >= 0 && any) {
+#else
     if (gl < ELL_W) {
 #pragma unroll
       for (int k = 0; k < SPL; ++k) {
@@ -485,6 +500,8 @@ __global__ void __launch_bounds__(Map<KP>::NT, 2)
       const int4 c1 = *reinterpret_cast<const int4*>(&s_ci[b][grp][4]);
       const int cc[ELL_W] = {c0.x & (ELL_LONG - 1), c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
       const double2* vp = reinterpret_cast<const double2*>(&s_cv[b][grp][0]);
+      const int c0x = c0.x;
+#endif
       double a[CPL];
 #pragma unroll
       for (int k = 0; k < CPL; ++k) a[k] = 0.0;
@@ -510,14 +527,18 @@ __global__ void __launch_bounds__(Map<KP>::NT, 2)
         // consume the batch last-issued first (slot order 7..0)
 #pragma unroll
         for (int k2 = ELL_HB / 2 - 1; k2 >= 0; --k2) {
+#if HF_SLOT_SHFL
+          const double2 vv = make_double2(vs[bt * ELL_HB + 2 * k2], vs[bt * ELL_HB + 2 * k2 + 1]);
+#else
           const double2 vv = vp[bt * ELL_HB / 2 + k2];
+#endif
 #pragma unroll
           for (int q = 0; q < CPL; ++q) a[q] = __fma_rn(vv.y, g[2 * k2 + 1][q], a[q]);
 #pragma unroll
           for (int q = 0; q < CPL; ++q) a[q] = __fma_rn(vv.x, g[2 * k2][q], a[q]);
         }
       }
-      if (c0.x & ELL_LONG) {  // entries 8.. of a long row, in order
+      if (c0x & ELL_LONG) {  // entries 8.. of a long row, in order
         const int st = __ldg(A.indptr + row), en = __ldg(A.indptr + row + 1);
         for (int j = st + ELL_W; j < en; ++j) {
           const int ce = __ldg(A.indices + j);

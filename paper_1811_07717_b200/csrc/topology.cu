@@ -280,6 +280,81 @@ TopoWs carve_topo(void* base, int n, int m, int ncols) {
 }
 }  // namespace
 
+namespace hf {
+namespace topo {
+// ---------------------------------------------------------------- electrodes / ground
+// Centroids of boundary triangles, numpy's mean of 3 rows: ((a + b) + c) / 3
+// (ElectrodeSet.from_centers, fem.py:163).
+__global__ void k_tri_centroids(const double* __restrict__ nodes, const int32_t* __restrict__ tri,
+                                int nt, double* __restrict__ cent) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  const int a = tri[3 * (size_t)t], b = tri[3 * (size_t)t + 1], c = tri[3 * (size_t)t + 2];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    cent[3 * (size_t)t + r] =
+        __ddiv_rn(__dadd_rn(__dadd_rn(nodes[3 * (size_t)a + r], nodes[3 * (size_t)b + r]),
+                            nodes[3 * (size_t)c + r]),
+                  3.0);
+}
+
+__global__ void k_mark_nodes(const int32_t* __restrict__ tri, int nt, unsigned bit,
+                             unsigned* __restrict__ mark) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (size_t)nt * 3) return;
+  atomicOr(&mark[tri[t]], bit);
+}
+
+__global__ void k_first_free(int n, const unsigned* __restrict__ mark, int* __restrict__ best) {
+  const int v = blockIdx.x * blockDim.x + threadIdx.x;
+  if (v < n && mark[v] == 1u) atomicMin(best, v);
+}
+
+}  // namespace topo
+}  // namespace hf
+
+extern "C" int hf_triangle_centroids(const double* nodes, const int32_t* tri, int32_t n_tri,
+                                     double* cent, void* stream) {
+  if (n_tri < 0 || (n_tri > 0 && (!nodes || !tri || !cent))) {
+    hf::set_error("hf_triangle_centroids: bad argument");
+    return HF_ERR_ARG;
+  }
+  if (n_tri == 0) return HF_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  hf::topo::k_tri_centroids<<<(n_tri + 255) / 256, 256, 0, s>>>(nodes, tri, n_tri, cent);
+  HF_LAUNCH_CHECK();
+  hf::count_launches(1);
+  return HF_OK;
+}
+
+extern "C" size_t hf_ground_node_workspace_bytes(int32_t n) { return 4 * ((size_t)n + 2) + 256; }
+
+extern "C" int hf_ground_node(const int32_t* bfaces, int32_t n_bfaces, const int32_t* etri,
+                              int32_t n_etri, int32_t n, void* ws, int32_t* ground, void* stream) {
+  if (!bfaces || !ws || !ground || n <= 0 || n_bfaces < 0 || n_etri < 0 || (n_etri > 0 && !etri)) {
+    hf::set_error("hf_ground_node: bad argument");
+    return HF_ERR_ARG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  unsigned* mark = reinterpret_cast<unsigned*>(ws);
+  int* best = reinterpret_cast<int*>(mark + n + 1);
+  HF_CUDA(cudaMemsetAsync(mark, 0, sizeof(unsigned) * (n + 1), s));
+  const int big = 0x7f7f7f7f;  // > any int32 node index this ABI accepts
+  HF_CUDA(cudaMemsetAsync(best, 0x7f, sizeof(int), s));
+  if (n_bfaces)
+    hf::topo::k_mark_nodes<<<(3 * n_bfaces + 255) / 256, 256, 0, s>>>(bfaces, n_bfaces, 1u, mark);
+  if (n_etri)
+    hf::topo::k_mark_nodes<<<(3 * n_etri + 255) / 256, 256, 0, s>>>(etri, n_etri, 2u, mark);
+  hf::topo::k_first_free<<<(n + 255) / 256, 256, 0, s>>>(n, mark, best);
+  HF_LAUNCH_CHECK();
+  hf::count_launches(1 + (n_bfaces > 0) + (n_etri > 0));
+  int h = big;
+  HF_CUDA(cudaMemcpyAsync(&h, best, sizeof(int), cudaMemcpyDeviceToHost, s));
+  HF_CUDA(cudaStreamSynchronize(s));
+  *ground = (h == big) ? -1 : h;
+  return HF_OK;
+}
+
 extern "C" size_t hf_topology_workspace_bytes(int32_t n, int32_t m, int32_t ncols) {
   return carve_topo(nullptr, n, m, ncols).bytes;
 }

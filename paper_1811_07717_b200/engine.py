@@ -59,7 +59,9 @@ class EegEngine:
             B, C, R = model.assemble_B_C_R(mesh, electrodes)
         self.L = B.shape[1]
         self.n = mesh.n_nodes if hasattr(mesh, "n_nodes") else len(mesh.nodes)
-        self.ground = model.ground_node(mesh, electrodes)
+        from .topology import ground_node_device
+
+        self.ground = ground_node_device(mesh, electrodes)
         tri, coef = model.electrode_contacts(electrodes)
         self.etri = torch.from_numpy(np.ascontiguousarray(tri, dtype=np.int32)).to(dev)
         self.ecoef = torch.from_numpy(np.ascontiguousarray(coef, dtype=np.float64)).to(dev)

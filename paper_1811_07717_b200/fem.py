@@ -17,7 +17,7 @@ import torch
 from . import _native as N
 from .device import DeviceCsr, device, to_device
 from .errors import AssemblyError
-from .model import ground_node, electrode_contacts
+from .model import electrode_contacts
 
 
 def _sigma_arg(mesh, sigma, elements):
@@ -140,7 +140,9 @@ def assemble_A_device(mesh, electrodes, ground=True):
     tri, coef = electrode_contacts(electrodes)
     g = -1
     if ground and electrodes.count:
-        g = ground_node(mesh, electrodes)
+        from .topology import ground_node_device
+
+        g = ground_node_device(mesh, electrodes)
     dev = dm.nodes.device
     et = torch.from_numpy(np.ascontiguousarray(tri, dtype=np.int32)).to(dev) if len(tri) else None
     ec = torch.from_numpy(np.ascontiguousarray(coef, dtype=np.float64)).to(dev) if len(tri) else None

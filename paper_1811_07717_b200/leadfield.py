@@ -102,7 +102,7 @@ def nearest_center_device(cc, centers):
     Cc = torch.from_numpy(np.ascontiguousarray(centers, dtype=np.float64)).to(dev)
     owner = torch.empty(max(len(cc), 1), dtype=torch.int32, device=dev)
     N.check("hf_nearest_center", N.lib.hf_nearest_center(
-        N.ptr(P), len(cc), N.ptr(Cc), len(centers), N.ptr(owner), N.stream_handle()))
+        N.ptr(P), len(cc), N.ptr(Cc), len(centers), N.ptr(owner), None, N.stream_handle()))
     return owner[: len(cc)].cpu().numpy().astype(np.int64)
 
 

@@ -108,15 +108,23 @@ def eeg_problem(name="c2", n_electrodes=None, n_sources=None, h=None, seed=1, de
         raise ValueError(name)
     mesh = sphere_mesh(radii, cond, h)
     if device:  # boundary faces and G' from the device kernels (topology.py)
-        from .topology import assemble_Gt_device, boundary_triangles_device
+        from .topology import assemble_Gt_device, boundary_triangles_device, electrodes_from_centers
 
         mesh._boundary = boundary_triangles_device(mesh)
-    el = model.ElectrodeSet.from_centers(mesh, fibonacci_sphere_points(L, radii[-1]), radius=rad,
-                                         impedances=1e3)
+    centers = fibonacci_sphere_points(L, radii[-1])
+    if device:  # nearest-centre coverage on the device (topology.electrodes_from_centers)
+        el = electrodes_from_centers(mesh, centers, radius=rad, impedances=1e3)
+    else:
+        el = model.ElectrodeSet.from_centers(mesh, centers, radius=rad, impedances=1e3)
     src = model.place_sources(mesh, [0], S, seed=seed)
     G = None
     if with_G:
         G = assemble_Gt_device(mesh, src) if device else model.assemble_G(mesh, src)
     B, C, R = model.assemble_B_C_R(mesh, el)
-    g = model.ground_node(mesh, el)
+    if device:
+        from .topology import ground_node_device
+
+        g = ground_node_device(mesh, el)
+    else:
+        g = model.ground_node(mesh, el)
     return EegProblem(mesh, el, src, G, B, C, R, g, name)

@@ -84,3 +84,30 @@ def test_leadfield_with_device_G(topo):
     lf = eng.build(to_host=True)
     ref = fx["LF"]
     assert np.linalg.norm(lf - ref) / np.linalg.norm(ref) <= 1e-6
+
+
+@pytest.mark.parametrize("name", ["sphere_small.npz", "layered_h12.npz", "c1.npz"])
+def test_electrodes_and_ground_on_device_match_reference(cuda, name):
+    """ElectrodeSet.from_centers (fem.py:157-173) and ground_node (fem.py:188-194)
+    on the device: the reference's triangle sets and grounding node."""
+    import numpy as np
+
+    from paper_1811_07717_b200 import model, synthetic
+    from paper_1811_07717_b200.topology import (boundary_triangles_device, electrodes_from_centers,
+                                                ground_node_device)
+    from tests.fixtures import electrodes_from_fixture, load, mesh_from_fixture
+
+    fx = load(name)
+    mesh = mesh_from_fixture(fx)
+    mesh._boundary = boundary_triangles_device(mesh)
+    ref = electrodes_from_fixture(mesh, fx)
+    L = ref.count
+    radius = {"sphere_small.npz": 0.05, "layered_h12.npz": 0.014, "c1.npz": 0.014}[name]
+    R = 0.1 if name == "sphere_small.npz" else 0.092
+    el = electrodes_from_centers(mesh, synthetic.fibonacci_sphere_points(L, R), radius, fx["impedances"])
+    host = model.ElectrodeSet.from_centers(mesh, synthetic.fibonacci_sphere_points(L, R), radius,
+                                           fx["impedances"])
+    for a, b, c in zip(el.triangle_ids, ref.triangle_ids, host.triangle_ids):
+        np.testing.assert_array_equal(a, b)
+        np.testing.assert_array_equal(a, c)
+    assert ground_node_device(mesh, el) == int(fx["ground"]) == model.ground_node(mesh, el)

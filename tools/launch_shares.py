@@ -6,7 +6,7 @@ import re
 import sys
 
 
-def main(path, out):
+def main(path, out, header="one full C2 LF build (tools/one_step.py between cudaProfilerStart/Stop)"):
     txt = open(path).read()
     rows = list(csv.DictReader(io.StringIO(txt[txt.index('"ID"'):])))
     tot = collections.defaultdict(float)
@@ -23,10 +23,8 @@ def main(path, out):
         cnt[name] += 1
     total = sum(tot.values())
     with open(out, "w") as f:
-        f.write("# ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 python bench.py "
-                "--steps 1 --warmup 0 --no-cpu-baseline --no-e2e\n")
-        f.write("# first 1500 launches of one C2 LF build (assembly + the first PCG rounds of batch 1); "
-                "cold-cache, serialised\n")
+        f.write("# ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none\n")
+        f.write(f"# {header}; per-launch times are cold-cache and serialised\n")
         f.write(f"# total {total:.2f} ms over {sum(cnt.values())} launches\n")
         f.write("kernel,launches,total_ms,share_pct,avg_us\n")
         for k in sorted(tot, key=tot.get, reverse=True):
@@ -34,4 +32,4 @@ def main(path, out):
 
 
 if __name__ == "__main__":
-    main(sys.argv[1], sys.argv[2])
+    main(*sys.argv[1:])
