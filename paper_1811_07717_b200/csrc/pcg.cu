@@ -103,20 +103,35 @@ struct Ctl {
   int* pbuf;  // per column: ring slot of its p once it stops running
 };
 
-template <int KP>
-struct Map {
-  static_assert(KP >= 2 && KP <= 64 && (KP & (KP - 1)) == 0, "kp in {2,...,64}");
-  // columns per lane: one 256/128/64-bit access; kp <= 16 keeps 1 column per lane
-  // so a reducing kernel still runs 16 lanes per row (512 threads at kp = 16)
-  static constexpr int CPL = (KP >= 64) ? 4 : (KP == 32 ? 2 : 1);
+// Thread layout of a kernel at batch width KP with CPL columns per lane: one row
+// group of LPR lanes per tile row, so a reducing kernel runs 32 x LPR threads.
+// Kernels may pick different CPL: the reduction order only depends on the tile
+// and row-group structure, not on how a row's columns are split over lanes.
+template <int KP_, int CPL_>
+struct Lay {
+  static_assert(KP_ >= 2 && KP_ <= 64 && (KP_ & (KP_ - 1)) == 0, "kp in {2,...,64}");
+  static constexpr int KP = KP_;
+  static constexpr int CPL = CPL_;
   static constexpr int LPR = KP / CPL;            // lanes per row
-  static constexpr int NT = TR * LPR;             // threads of a reducing kernel: one row group per tile row
+  static constexpr int NT = TR * LPR;             // threads of a reducing kernel
   static constexpr int NW = NT / 32;              // warps of a reducing kernel
   static constexpr int SPL = LPR >= ELL_W ? 1 : ELL_W / LPR;  // ELL slots held per lane
-  // tiles in flight per thread in the streaming kernels (register budget: 64)
-  static constexpr int U = (CPL == 4) ? 1 : (CPL == 2 ? 2 : 4);
   static constexpr int RED = (NW * KP * 2 > RSEG * KP * 2) ? NW * KP * 2 : RSEG * KP * 2;
 };
+
+// Streaming kernels: one 256/128/64-bit access per lane; kp <= 16 keeps 1 column
+// per lane so a reducing kernel still runs 16 lanes per row (512 threads at kp = 16).
+template <int KP>
+struct Map : Lay<KP, (KP >= 64) ? 4 : (KP == 32 ? 2 : 1)> {
+  using B = Lay<KP, (KP >= 64) ? 4 : (KP == 32 ? 2 : 1)>;
+  // tiles in flight per thread in the streaming kernels (register budget: 64)
+  static constexpr int U = (B::CPL == 4) ? 1 : (B::CPL == 2 ? 2 : 4);
+};
+
+// The SpMM moves at least 128 bits per lane per gather (kp = 16: 8 lanes per row,
+// two tiles per step in flight, see k_spmm).
+template <int KP>
+using SpmmLay = Lay<KP, (KP >= 64) ? 4 : 2>;
 
 __host__ __device__ inline int n_tiles(int n) { return (n + TR - 1) / TR; }
 
@@ -183,10 +198,10 @@ __device__ __forceinline__ double dot_acc(double acc, double a, double b) { retu
 // Block partials: v[q][k] is this thread's running sum (its row group, column
 // glane*CPL + k).  Balanced tree over the block's 32 row groups; the block's
 // partial row goes to part{q}[blockIdx.x * KP + col].
-template <int KP, int NV>
-__device__ __forceinline__ void block_partials(double (&v)[NV][Map<KP>::CPL], double* sm,
+template <class M, int NV>
+__device__ __forceinline__ void block_partials(double (&v)[NV][M::CPL], double* sm,
                                                const Ctl& c) {
-  using M = Map<KP>;
+  constexpr int KP = M::KP;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int glane = tid % M::LPR;
 #pragma unroll
@@ -223,9 +238,9 @@ __device__ __forceinline__ void block_partials(double (&v)[NV][Map<KP>::CPL], do
 // The reduction is on the critical path of every round (the next kernel waits
 // for it), so each thread keeps 8 loads per quantity in flight instead of
 // walking its segment one L2 round trip at a time.
-template <int KP, int NV>
+template <class M, int NV>
 __device__ __forceinline__ bool last_block_reduce(const Ctl& c, double* sm, double* tot) {
-  using M = Map<KP>;
+  constexpr int KP = M::KP;
   __shared__ int s_last;
   __threadfence();
   __syncthreads();
@@ -323,8 +338,8 @@ __global__ void __launch_bounds__(Map<KP>::NT)
     st_cols<M::CPL>(R + o, b);
     st_cols<M::CPL>(P + o, z);
   }
-  block_partials<KP, 2>(v, sm, c);
-  if (!last_block_reduce<KP, 2>(c, sm, tot)) return;
+  block_partials<M, 2>(v, sm, c);
+  if (!last_block_reduce<M, 2>(c, sm, tot)) return;
   int st = -1;
   if (tid < KP) {
     const int j = tid;
@@ -364,9 +379,6 @@ __global__ void __launch_bounds__(Map<KP>::NT)
 constexpr int ELL_LONG = 1 << 30;
 constexpr int ELL_OPT = 5;  // first slot gathered only when it holds an entry
 constexpr int ELL_HB = 4;   // gathers in flight per batch
-#ifndef HF_SLOT_SHFL
-#define HF_SLOT_SHFL 0
-#endif
 
 __global__ void k_ell_fill(int n, const int32_t* __restrict__ indptr,
                            const int32_t* __restrict__ indices, const double* __restrict__ val,
@@ -415,16 +427,19 @@ struct Ell {
 enum { MODE_PQ = 0, MODE_RESID = 1 };
 
 template <int KP, int MODE>
-__global__ void __launch_bounds__(Map<KP>::NT, 2)
+__global__ void __launch_bounds__(SpmmLay<KP>::NT, 2)
     k_spmm(Ctl c, Ell A, const double* __restrict__ V, const double* __restrict__ Bv,
            double* __restrict__ Q) {
-  using M = Map<KP>;
+  using M = SpmmLay<KP>;
   constexpr int CPL = M::CPL, LPR = M::LPR, SPL = M::SPL;
+  // tiles per step: narrow batches move few bytes per gather, so a row group keeps
+  // two rows' gathers in flight (the rows are still summed in tile order)
+  constexpr int UT = (KP <= 16) ? 2 : 1;
   __shared__ double sm[M::RED];
   __shared__ double tot[KP];
   __shared__ int s_act[KP];
-  __shared__ __align__(16) int s_ci[2][TR][ELL_W];
-  __shared__ __align__(16) double s_cv[2][TR][ELL_W];
+  __shared__ __align__(16) int s_ci[2][UT][TR][ELL_W];
+  __shared__ __align__(16) double s_cv[2][UT][TR][ELL_W];
   if (MODE == MODE_PQ && c.summary[SUM_RUN] == 0) return;
   if (MODE == MODE_RESID && c.summary[SUM_CHECK] == 0) {
     if (blockIdx.x == 0 && threadIdx.x == 0) c.summary[SUM_REPLACE] = 0;
@@ -464,123 +479,143 @@ __global__ void __launch_bounds__(Map<KP>::NT, 2)
       }
     }
   };
-  int t = blockIdx.x;
-  int row = tile_row(t);
-  int ci[SPL];
-  double cv[SPL];
-  load_slots(row, ci, cv);
-  int b = 0;
-  for (; t < nt; t += c.G, b ^= 1) {
-    const int rowN = tile_row(t + c.G);
-    int ciN[SPL];
-    double cvN[SPL];
-    load_slots(rowN, ciN, cvN);  // next tile's slots in flight during this one
-#if HF_SLOT_SHFL
-    int cc[ELL_W];
-    double vs[ELL_W];
+  int row[UT], ci[UT][SPL];
+  double cv[UT][SPL];
 #pragma unroll
-    for (int e = 0; e < ELL_W; ++e) {  // slot e sits in lane e % LPR, register e / LPR
-      cc[e] = __shfl_sync(FULL, ci[e / LPR], e % LPR, LPR);
-      vs[e] = __shfl_sync(FULL, cv[e / LPR], e % LPR, LPR);
+  for (int u = 0; u < UT; ++u) {
+    row[u] = tile_row(blockIdx.x + u * c.G);
+    load_slots(row[u], ci[u], cv[u]);
+  }
+  int b = 0;
+  for (int t = blockIdx.x; t < nt; t += UT * c.G, b ^= 1) {
+    int rowN[UT], ciN[UT][SPL];
+    double cvN[UT][SPL];
+#pragma unroll
+    for (int u = 0; u < UT; ++u) {  // next step's slots in flight during this one
+      rowN[u] = tile_row(t + (UT + u) * c.G);
+      load_slots(rowN[u], ciN[u], cvN[u]);
     }
-    const int c0x = cc[0];
-    cc[0] &= ELL_LONG - 1;
-    if (row >= 0 && any) {
-#else
     if (gl < ELL_W) {
 #pragma unroll
-      for (int k = 0; k < SPL; ++k) {
-        s_ci[b][grp][gl + k * LPR] = ci[k];
-        s_cv[b][grp][gl + k * LPR] = cv[k];
-      }
+      for (int u = 0; u < UT; ++u)
+#pragma unroll
+        for (int k = 0; k < SPL; ++k) {
+          s_ci[b][u][grp][gl + k * LPR] = ci[u][k];
+          s_cv[b][u][grp][gl + k * LPR] = cv[u][k];
+        }
     }
-    if (LPR < 32) __syncwarp();
-    if (row >= 0 && any) {
-      const int4 c0 = *reinterpret_cast<const int4*>(&s_ci[b][grp][0]);
-      const int4 c1 = *reinterpret_cast<const int4*>(&s_ci[b][grp][4]);
-      const int cc[ELL_W] = {c0.x & (ELL_LONG - 1), c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-      const double2* vp = reinterpret_cast<const double2*>(&s_cv[b][grp][0]);
-      const int c0x = c0.x;
-#endif
-      double a[CPL];
+    __syncwarp();
+    int cc[UT][ELL_W], c0x[UT];
+    bool live[UT];
 #pragma unroll
-      for (int k = 0; k < CPL; ++k) a[k] = 0.0;
-      double g0[CPL];  // slot 0's gather: p_i when slot 0 is the diagonal
+    for (int u = 0; u < UT; ++u) {
+      const int4 c0 = *reinterpret_cast<const int4*>(&s_ci[b][u][grp][0]);
+      const int4 c1 = *reinterpret_cast<const int4*>(&s_ci[b][u][grp][4]);
+      c0x[u] = c0.x;
+      cc[u][0] = c0.x & (ELL_LONG - 1);
+      cc[u][1] = c0.y;
+      cc[u][2] = c0.z;
+      cc[u][3] = c0.w;
+      cc[u][4] = c1.x;
+      cc[u][5] = c1.y;
+      cc[u][6] = c1.z;
+      cc[u][7] = c1.w;
+      live[u] = row[u] >= 0 && any;
+    }
+    double a[UT][CPL], g0[UT][CPL];  // g0: slot 0's gather, p_i when slot 0 is the diagonal
+    bool anylive = false;
 #pragma unroll
-      for (int bt = ELL_W / ELL_HB - 1; bt >= 0; --bt) {
-        double g[ELL_HB][CPL];
+    for (int u = 0; u < UT; ++u) {
+      anylive |= live[u];
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) a[u][k] = 0.0;
+    }
+    if (anylive) {
+#pragma unroll
+    for (int bt = ELL_W / ELL_HB - 1; bt >= 0; --bt) {
+      double g[UT][ELL_HB][CPL];
+#pragma unroll
+      for (int u = 0; u < UT; ++u)
 #pragma unroll
         for (int k = 0; k < ELL_HB; ++k) {
           const int e = bt * ELL_HB + k;
           if (e >= ELL_OPT) {  // optional slot: zero when empty
 #pragma unroll
-            for (int q = 0; q < CPL; ++q) g[k][q] = 0.0;
-            if (cc[e] >= 0) ldg_cols<CPL>(Vl + (size_t)cc[e] * KP, g[k]);
-          } else {
-            ldg_cols<CPL>(Vl + (size_t)(unsigned)cc[e] * KP, g[k]);
+            for (int q = 0; q < CPL; ++q) g[u][k][q] = 0.0;
+            if (live[u] && cc[u][e] >= 0) ldg_cols<CPL>(Vl + (size_t)cc[u][e] * KP, g[u][k]);
+          } else if (live[u]) {
+            ldg_cols<CPL>(Vl + (size_t)(unsigned)cc[u][e] * KP, g[u][k]);
           }
         }
+#pragma unroll
+      for (int u = 0; u < UT; ++u) {
         if (bt == 0) {
 #pragma unroll
-          for (int q = 0; q < CPL; ++q) g0[q] = g[0][q];
+          for (int q = 0; q < CPL; ++q) g0[u][q] = g[u][0][q];
         }
+        const double2* vp = reinterpret_cast<const double2*>(&s_cv[b][u][grp][0]);
         // consume the batch last-issued first (slot order 7..0)
 #pragma unroll
         for (int k2 = ELL_HB / 2 - 1; k2 >= 0; --k2) {
-#if HF_SLOT_SHFL
-          const double2 vv = make_double2(vs[bt * ELL_HB + 2 * k2], vs[bt * ELL_HB + 2 * k2 + 1]);
-#else
           const double2 vv = vp[bt * ELL_HB / 2 + k2];
-#endif
 #pragma unroll
-          for (int q = 0; q < CPL; ++q) a[q] = __fma_rn(vv.y, g[2 * k2 + 1][q], a[q]);
+          for (int q = 0; q < CPL; ++q) a[u][q] = __fma_rn(vv.y, g[u][2 * k2 + 1][q], a[u][q]);
 #pragma unroll
-          for (int q = 0; q < CPL; ++q) a[q] = __fma_rn(vv.x, g[2 * k2][q], a[q]);
+          for (int q = 0; q < CPL; ++q) a[u][q] = __fma_rn(vv.x, g[u][2 * k2][q], a[u][q]);
         }
       }
-      if (c0x & ELL_LONG) {  // entries 8.. of a long row, in order
-        const int st = __ldg(A.indptr + row), en = __ldg(A.indptr + row + 1);
+    }
+    }
+#pragma unroll
+    for (int u = 0; u < UT; ++u) {  // epilogues in tile order (the canonical dot order)
+      if (!live[u]) continue;
+      const int r = row[u];
+      if (c0x[u] & ELL_LONG) {  // entries 8.. of a long row, in order
+        const int st = __ldg(A.indptr + r), en = __ldg(A.indptr + r + 1);
         for (int j = st + ELL_W; j < en; ++j) {
           const int ce = __ldg(A.indices + j);
           const double ve = __ldg(A.val + j);
           double q2[CPL];
           ldg_cols<CPL>(Vl + (size_t)ce * KP, q2);
 #pragma unroll
-          for (int q = 0; q < CPL; ++q) a[q] = __fma_rn(ve, q2[q], a[q]);
+          for (int q = 0; q < CPL; ++q) a[u][q] = __fma_rn(ve, q2[q], a[u][q]);
         }
       }
-      const size_t o = (size_t)row * KP + gl * CPL;
+      const size_t o = (size_t)r * KP + gl * CPL;
       if constexpr (MODE == MODE_PQ) {
-        st_cols<CPL>(Q + o, a);
+        st_cols<CPL>(Q + o, a[u]);
         double pr[CPL];
-        if (cc[0] == row) {
+        if (cc[u][0] == r) {
 #pragma unroll
-          for (int q = 0; q < CPL; ++q) pr[q] = g0[q];
+          for (int q = 0; q < CPL; ++q) pr[q] = g0[u][q];
         } else {
           ldg_cols<CPL>(V + o, pr);
         }
 #pragma unroll
-        for (int q = 0; q < CPL; ++q) v[0][q] = __fma_rn(__dmul_rn(pr[q], a[q]), m[q], v[0][q]);
+        for (int q = 0; q < CPL; ++q) v[0][q] = __fma_rn(__dmul_rn(pr[q], a[u][q]), m[q], v[0][q]);
       } else {
-        double bb[CPL], s[CPL];
+        double bb[CPL], sres[CPL];
         ld_cols<CPL>(Bv + o, bb);
 #pragma unroll
         for (int q = 0; q < CPL; ++q) {
-          s[q] = __dsub_rn(bb[q], a[q]);
-          if (act[q]) v[0][q] = dot_acc(v[0][q], s[q], s[q]);
+          sres[q] = __dsub_rn(bb[q], a[u][q]);
+          if (act[q]) v[0][q] = dot_acc(v[0][q], sres[q], sres[q]);
         }
-        st_cols<CPL>(Q + o, s);
+        st_cols<CPL>(Q + o, sres);
       }
     }
-    row = rowN;
 #pragma unroll
-    for (int k = 0; k < SPL; ++k) {
-      ci[k] = ciN[k];
-      cv[k] = cvN[k];
+    for (int u = 0; u < UT; ++u) {
+      row[u] = rowN[u];
+#pragma unroll
+      for (int k = 0; k < SPL; ++k) {
+        ci[u][k] = ciN[u][k];
+        cv[u][k] = cvN[u][k];
+      }
     }
   }
-  block_partials<KP, 1>(v, sm, c);
-  if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
+  block_partials<M, 1>(v, sm, c);
+  if (!last_block_reduce<M, 1>(c, sm, tot)) return;
   if constexpr (MODE == MODE_PQ) {
     if (tid < KP && s_act[tid]) c.alpha[tid] = c.rz[tid] / tot[tid];
   } else {
@@ -679,8 +714,8 @@ __global__ void __launch_bounds__(Map<KP>::NT, 2)
       }
     }
   }
-  block_partials<KP, 2>(v, sm, c);
-  if (!last_block_reduce<KP, 2>(c, sm, tot)) return;
+  block_partials<M, 2>(v, sm, c);
+  if (!last_block_reduce<M, 2>(c, sm, tot)) return;
   int xm = 0, pm = 0, st = -1;
   if (tid < KP) {
     const int j = tid;
@@ -894,8 +929,8 @@ __global__ void __launch_bounds__(Map<KP>::NT, 2)
       st_cols<M::CPL>(R + o, r);
     }
   }
-  block_partials<KP, 1>(v, sm, c);
-  if (!last_block_reduce<KP, 1>(c, sm, tot)) return;
+  block_partials<M, 1>(v, sm, c);
+  if (!last_block_reduce<M, 1>(c, sm, tot)) return;
   int st = -1;
   if (tid < KP) {
     const int j = tid;
@@ -1070,7 +1105,7 @@ inline void launch_round(const Grids& g0, const Layout& L, double* X, int r, cud
     k->xmask = L.xmask + (size_t)slot * KP;
   }
   double* Pc = L.P + (size_t)slot * nk;
-  k_spmm<KP, MODE_PQ><<<g.c.G, M::NT, 0, q>>>(g.c, g.ell, Pc, nullptr, L.Q);
+  k_spmm<KP, MODE_PQ><<<g.c.G, SpmmLay<KP>::NT, 0, q>>>(g.c, g.ell, Pc, nullptr, L.Q);
   if (ev) cudaEventRecord(ev[1], q);
   k_update_r<KP><<<g.c.G, M::NT, 0, q>>>(g.c, L.Q, L.R);
   if (ev) cudaEventRecord(ev[2], q);
@@ -1088,7 +1123,7 @@ inline void launch_check(const Grids& g0, const Layout& L, const double* B, doub
   using M = Map<KP>;
   Grids g = g0;
   g.c.xmask = L.xmask + (size_t)XD * KP;  // scratch: the round slots stay untouched
-  k_spmm<KP, MODE_RESID><<<g.c.G, M::NT, 0, q>>>(g.c, g.ell, X, B, L.Q);
+  k_spmm<KP, MODE_RESID><<<g.c.G, SpmmLay<KP>::NT, 0, q>>>(g.c, g.ell, X, B, L.Q);
   k_replace<KP><<<g.c.G, M::NT, 0, q>>>(g.c, L.Q, L.R);
   k_replace_p<KP><<<g.crp.G, M::NT, 0, q>>>(g.crp, L.P, (size_t)g.c.n * KP, L.R);
 }
