@@ -31,6 +31,8 @@
  *   hf_nearest_center      leadfield.py:96-99  build_dof_map: owner = argmin ||c_i - centre_j||
  *                          fem.py:157-173      ElectrodeSet.from_centers (nearest centre + distance)
  *   hf_triangle_centroids  fem.py:163          boundary-triangle centroids of from_centers
+ *   hf_tet_centroids       leadfield.py:96     build_dof_map's element centroids
+ *   hf_dof_partition       leadfield.py:99-100 build_dof_map's sets: cand[owner == k] for every k
  *   hf_ground_node         fem.py:188-194      ground_node
  *   hf_locate              geometry.py:147-374 Segmentation.locate (ray-parity point location)
  *   hf_grid_tets           meshgen.py:205-223  generate_mesh's Kuhn grid + element centroids
@@ -256,6 +258,18 @@ int hf_nearest_center(const double* points, int32_t n_points, const double* cent
 /* dist (device n_points f64, or NULL): the winning distance, as np.linalg.norm
  * computes it — ElectrodeSet.from_centers' coverage test d <= radius
  * (fem.py:164-167) uses the same routine on boundary-triangle centroids. */
+
+/* Element centroids (((a + b) + c) + d) / 4 (TetMesh.centroids' numpy rounding) of
+ * elems[0..count) (device int32, or NULL for elements 0..count-1); cent device count x 3. */
+int hf_tet_centroids(const double* nodes, const int32_t* tetra, const int32_t* elems, int32_t count,
+                     double* cent, void* stream);
+
+/* build_dof_map's sets (leadfield.py:99-100): sorted_cand = cand stably sorted by owner
+ * (each set keeps ascending element order), set_ptr[k] = first position of set k
+ * (n_sets + 1 entries).  All device int32; ws: hf_dof_partition_workspace_bytes(n_cand). */
+size_t hf_dof_partition_workspace_bytes(int32_t n_cand);
+int hf_dof_partition(const int32_t* cand, const int32_t* owner, int32_t n_cand, int32_t n_sets,
+                     int32_t* sorted_cand, int32_t* set_ptr, void* ws, size_t ws_bytes, void* stream);
 
 /* Centroids ((a + b) + c) / 3 of n_tri triangles (device n_tri x 3 int32 node ids),
  * numpy's mean over 3 rows (fem.py:163).  cent device n_tri x 3 f64. */

@@ -65,6 +65,9 @@ def _load():
         "hf_whitney_gt": (C.c_int, [P, P, I32, I32, P, I32, P, P, P, P, C.POINTER(I64), P, SZ, P]),
         "hf_nearest_center": (C.c_int, [P, I32, P, I32, P, P, P]),
         "hf_triangle_centroids": (C.c_int, [P, P, I32, P, P]),
+        "hf_tet_centroids": (C.c_int, [P, P, P, I32, P, P]),
+        "hf_dof_partition_workspace_bytes": (SZ, [I32]),
+        "hf_dof_partition": (C.c_int, [P, P, I32, I32, P, P, P, SZ, P]),
         "hf_ground_node_workspace_bytes": (SZ, [I32]),
         "hf_ground_node": (C.c_int, [P, I32, P, I32, I32, P, C.POINTER(I32), P]),
         "hf_locate": (C.c_int, [C.POINTER(HfSegmentation), P, I32, P, P]),
@@ -94,7 +97,8 @@ EXPORTED = ("hf_version", "hf_last_error", "hf_device_sm_count", "hf_launch_coun
             "hf_p1_assemble_workspace_bytes", "hf_p1_assemble_prepare", "hf_p1_assemble_fill",
             "hf_response_matrix", "hf_lf_tail", "hf_dense_lf", "hf_eit_sens_workspace_bytes", "hf_eit_sens",
             "hf_topology_workspace_bytes", "hf_boundary_faces", "hf_whitney_gt",
-            "hf_nearest_center", "hf_triangle_centroids", "hf_ground_node_workspace_bytes",
+            "hf_nearest_center", "hf_triangle_centroids", "hf_tet_centroids",
+            "hf_dof_partition_workspace_bytes", "hf_dof_partition", "hf_ground_node_workspace_bytes",
             "hf_ground_node", "hf_locate", "hf_grid_tets", "hf_mesh_compact_workspace_bytes",
             "hf_mesh_compact", "hf_apply_priorities", "hf_meg_workspace_bytes", "hf_meg_rhs",
             "hf_meg_primary")

@@ -98,3 +98,97 @@ extern "C" int hf_nearest_center(const double* points, int32_t n_points, const d
   count_launches(1);
   return HF_OK;
 }
+
+// ---------------------------------------------------------------- DOF map partition (next row #3)
+// The host steps of build_dof_map (leadfield.py:80-101) around the nearest-centre
+// search, on the device: element centroids with numpy's rounding
+// (mean over 4 corners = (((a + b) + c) + d) / 4, meshgen.py:TetMesh.centroids),
+// and the partition sets = cand[owner == k] for every k, as one stable radix sort
+// of the candidates by owner (ascending element order inside each set, as the
+// reference's boolean mask gives) plus the set offsets.
+#include <cub/device/device_radix_sort.cuh>
+
+namespace hf {
+namespace dof {
+
+__global__ void k_tet_centroids(const double* __restrict__ nodes, const int32_t* __restrict__ tetra,
+                                const int32_t* __restrict__ elems, int count,
+                                double* __restrict__ cent) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  const size_t e = elems ? (size_t)elems[i] : (size_t)i;
+  const int32_t* t = tetra + 4 * e;
+  const double* a = nodes + 3 * (size_t)t[0];
+  const double* b = nodes + 3 * (size_t)t[1];
+  const double* c = nodes + 3 * (size_t)t[2];
+  const double* d = nodes + 3 * (size_t)t[3];
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    cent[3 * (size_t)i + r] = __dmul_rn(__dadd_rn(__dadd_rn(__dadd_rn(a[r], b[r]), c[r]), d[r]), 0.25);
+}
+
+__global__ void k_set_bounds(const int32_t* __restrict__ sorted_owner, int n, int n_sets,
+                             int32_t* __restrict__ ptr) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k > n_sets) return;
+  int lo = 0, hi = n;  // first position with owner >= k
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (sorted_owner[mid] < k) lo = mid + 1; else hi = mid;
+  }
+  ptr[k] = lo;
+}
+
+}  // namespace dof
+}  // namespace hf
+
+extern "C" int hf_tet_centroids(const double* nodes, const int32_t* tetra, const int32_t* elems,
+                                int32_t count, double* cent, void* stream) {
+  if (count < 0 || (count > 0 && (!nodes || !tetra || !cent))) {
+    set_error("hf_tet_centroids: bad argument");
+    return HF_ERR_ARG;
+  }
+  if (count == 0) return HF_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  dof::k_tet_centroids<<<(count + 255) / 256, 256, 0, s>>>(nodes, tetra, elems, count, cent);
+  HF_LAUNCH_CHECK();
+  count_launches(1);
+  return HF_OK;
+}
+
+static size_t partition_sort_bytes(int32_t n) {
+  size_t tmp = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, n);
+  return tmp;
+}
+
+extern "C" size_t hf_dof_partition_workspace_bytes(int32_t n_cand) {
+  return partition_sort_bytes(n_cand) + 4 * ((size_t)n_cand + 64) + 512;
+}
+
+extern "C" int hf_dof_partition(const int32_t* cand, const int32_t* owner, int32_t n_cand,
+                                int32_t n_sets, int32_t* sorted_cand, int32_t* set_ptr, void* ws,
+                                size_t ws_bytes, void* stream) {
+  if (!cand || !owner || !sorted_cand || !set_ptr || !ws || n_cand < 0 || n_sets < 1) {
+    set_error("hf_dof_partition: bad argument");
+    return HF_ERR_ARG;
+  }
+  if (ws_bytes < hf_dof_partition_workspace_bytes(n_cand)) {
+    set_error("hf_dof_partition: workspace too small");
+    return HF_ERR_WORKSPACE;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Carve cv{reinterpret_cast<char*>(ws), 0, ws_bytes};
+  int32_t* sorted_owner = cv.take<int32_t>((size_t)n_cand + 1);
+  size_t tmp_bytes = partition_sort_bytes(n_cand);
+  void* tmp = cv.take<char>(tmp_bytes + 1);
+  int bits = 1;
+  while ((1 << bits) <= n_sets && bits < 31) ++bits;
+  HF_CUDA(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, owner, sorted_owner, cand, sorted_cand,
+                                          n_cand, 0, bits, s));
+  dof::k_set_bounds<<<(n_sets + 256) / 256, 256, 0, s>>>(sorted_owner, n_cand, n_sets, set_ptr);
+  HF_LAUNCH_CHECK();
+  count_launches(2);
+  return HF_OK;
+}

@@ -124,15 +124,15 @@ def build_dof_map(mesh, compartments, n_dofs, seed=0, chunk=8192, method="auto")
     rng = np.random.default_rng(seed)
     vols = mesh.volumes[cand]
     chosen = rng.choice(cand, size=n_dofs, replace=False, p=vols / vols.sum())
-    centroids = mesh.centroids()
-    centers = centroids[chosen]
-    cc = centroids[cand]
     if method == "auto":
         method = "device" if torch.cuda.is_available() else (
             "tree" if len(cand) * n_dofs > 5e7 else "dense")
     if method == "device":
-        owner = nearest_center_device(cc, centers)
-    elif method == "tree":
+        return _dof_map_device(mesh, cand, chosen)
+    centroids = mesh.centroids()
+    centers = centroids[chosen]
+    cc = centroids[cand]
+    if method == "tree":
         owner = _nearest_center_exact(cc, centers, chunk)
     else:
         owner = np.empty(len(cand), dtype=np.int64)
@@ -144,6 +144,42 @@ def build_dof_map(mesh, compartments, n_dofs, seed=0, chunk=8192, method="auto")
     bounds = np.searchsorted(owner[order], np.arange(n_dofs + 1))
     sets = tuple(cand[order[bounds[k]:bounds[k + 1]]] for k in range(n_dofs))
     return EitDofMap(element_sets=sets, centers=centers)
+
+
+def _dof_map_device(mesh, cand, chosen):
+    """Centroids (hf_tet_centroids), nearest centre (hf_nearest_center) and the
+    partition into sets (hf_dof_partition) on the device; only the reference's
+    random draw and the final split into per-DOF views run on the host.  The
+    device arrays stay attached to the map for dof_sensitivities_device."""
+    from .fem import DeviceMesh
+
+    dm = DeviceMesh.of(mesh)
+    dev = dm.nodes.device
+    st = N.stream_handle()
+    n_dofs = len(chosen)
+    cand_d = torch.from_numpy(cand.astype(np.int32)).to(dev)
+    cc = torch.empty((len(cand), 3), dtype=torch.float64, device=dev)
+    N.check("hf_tet_centroids", N.lib.hf_tet_centroids(N.ptr(dm.nodes), N.ptr(dm.tetra), N.ptr(cand_d),
+                                                       len(cand), N.ptr(cc), st))
+    chosen_d = torch.from_numpy(np.asarray(chosen, dtype=np.int32)).to(dev)
+    ctr = torch.empty((n_dofs, 3), dtype=torch.float64, device=dev)
+    N.check("hf_tet_centroids", N.lib.hf_tet_centroids(N.ptr(dm.nodes), N.ptr(dm.tetra), N.ptr(chosen_d),
+                                                       n_dofs, N.ptr(ctr), st))
+    owner = torch.empty(max(len(cand), 1), dtype=torch.int32, device=dev)
+    N.check("hf_nearest_center", N.lib.hf_nearest_center(N.ptr(cc), len(cand), N.ptr(ctr), n_dofs,
+                                                         N.ptr(owner), None, st))
+    sorted_d = torch.empty_like(cand_d)
+    ptr_d = torch.empty(n_dofs + 1, dtype=torch.int32, device=dev)
+    ws = torch.empty(N.lib.hf_dof_partition_workspace_bytes(len(cand)), dtype=torch.uint8, device=dev)
+    N.check("hf_dof_partition", N.lib.hf_dof_partition(N.ptr(cand_d), N.ptr(owner), len(cand), n_dofs,
+                                                       N.ptr(sorted_d), N.ptr(ptr_d), N.ptr(ws),
+                                                       ws.numel(), st))
+    elems = sorted_d.cpu().numpy().astype(np.int64)
+    ptr = ptr_d.cpu().numpy().astype(np.int64)
+    sets = tuple(np.split(elems, ptr[1:-1]))
+    dmap = EitDofMap(element_sets=sets, centers=ctr.cpu().numpy())
+    object.__setattr__(dmap, "_device", (sorted_d, ptr_d))
+    return dmap
 
 
 # ---------------------------------------------------------------- device system
@@ -283,13 +319,17 @@ def dof_sensitivities_device(mesh, dofs, ground, T, U, L, P):
     """Q (P x m_dofs x L, device) = T' K_m u_p for every DOF and pattern."""
     dm = DeviceMesh.of(mesh)
     dev = T.device
-    elems = np.concatenate([np.asarray(e, dtype=np.int64) for e in dofs.element_sets])
-    ptr = np.cumsum([0] + [len(e) for e in dofs.element_sets])
-    de = torch.from_numpy(elems.astype(np.int32)).to(dev)
-    dp = torch.from_numpy(ptr.astype(np.int32)).to(dev)
+    cached = getattr(dofs, "_device", None)
+    if cached is not None and cached[0].device == dev:  # built by _dof_map_device
+        de, dp = cached
+    else:
+        elems = np.concatenate([np.asarray(e, dtype=np.int64) for e in dofs.element_sets])
+        ptr = np.cumsum([0] + [len(e) for e in dofs.element_sets])
+        de = torch.from_numpy(elems.astype(np.int32)).to(dev)
+        dp = torch.from_numpy(ptr.astype(np.int32)).to(dev)
     nd = dofs.n_dofs
     Q = torch.empty((P, nd, L), dtype=torch.float64, device=dev)
-    ws = torch.empty(N.lib.hf_eit_sens_workspace_bytes(len(elems)), dtype=torch.uint8, device=dev)
+    ws = torch.empty(N.lib.hf_eit_sens_workspace_bytes(de.numel()), dtype=torch.uint8, device=dev)
     N.check("hf_eit_sens", N.lib.hf_eit_sens(
         N.ptr(dm.nodes), N.ptr(dm.tetra), N.ptr(de), N.ptr(dp), nd, int(ground), N.ptr(T),
         T.stride(0), L, N.ptr(U), U.stride(0), P, N.ptr(Q), N.ptr(ws), ws.numel(), N.stream_handle()))

@@ -186,3 +186,26 @@ def test_nearest_center_ties_take_first_index(eng):
     s = 2.0
     c2 = np.array([[np.sqrt(np.nextafter(s, 3)), 0, 0], [np.sqrt(s), 0, 0]])
     np.testing.assert_array_equal(nearest_center_device(base, c2), _dense_owner(base, c2))
+
+
+def test_tet_centroids_bitwise_and_partition(eng):
+    """hf_tet_centroids equals TetMesh.centroids() bit for bit (numpy's rounding of the
+    4-corner mean), and the device DOF map (centroids, nearest centre, partition) equals
+    the host path's sets on the C1 mesh."""
+    import torch
+
+    from paper_1811_07717_b200 import _native as N
+    from paper_1811_07717_b200.fem import DeviceMesh
+    from paper_1811_07717_b200.leadfield import build_dof_map
+    from tests.fixtures import mesh_from_fixture
+
+    mesh = mesh_from_fixture(load("c1.npz"))
+    dm = DeviceMesh.of(mesh)
+    out = torch.empty((mesh.n_elements, 3), dtype=torch.float64, device="cuda")
+    N.check("hf_tet_centroids", N.lib.hf_tet_centroids(N.ptr(dm.nodes), N.ptr(dm.tetra), None,
+                                                       mesh.n_elements, N.ptr(out), N.stream_handle()))
+    np.testing.assert_array_equal(out.cpu().numpy(), mesh.centroids())
+    dev = build_dof_map(mesh, [0, 1], 700, seed=5, method="device")
+    host = build_dof_map(mesh, [0, 1], 700, seed=5, method="tree")
+    np.testing.assert_array_equal(dev.centers, host.centers)
+    assert all(np.array_equal(a, b) for a, b in zip(dev.element_sets, host.element_sets))
