@@ -1,5 +1,5 @@
 """Short driver for ncu: build the C1/C2 system on the device and run a few PCG
-rounds through hf_pcg_profile (kernel names k_spmm_pq / k_update_r / k_update_xp),
+rounds through hf_pcg_profile (k_spmm / k_update_r / k_update_p, k_update_xring),
 or one full LF build (--build).  Never used for timing numbers."""
 import argparse
 import os
@@ -26,6 +26,6 @@ if args.build:
 else:
     import bench
 
-    print(bench.kernel_roofline(eng, A, rounds=args.rounds, config=args.config))
+    print(bench.kernel_roofline(eng.Bd, A, rounds=args.rounds, config=args.config))
 torch.cuda.synchronize()
 print("done")
