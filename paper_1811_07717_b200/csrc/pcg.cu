@@ -379,9 +379,6 @@ __global__ void __launch_bounds__(Map<KP>::NT)
 constexpr int ELL_LONG = 1 << 30;
 constexpr int ELL_OPT = 5;  // first slot gathered only when it holds an entry
 constexpr int ELL_HB = 4;   // gathers in flight per batch
-#ifndef HF_SLOT_LDG
-#define HF_SLOT_LDG 0
-#endif
 
 __global__ void k_ell_fill(int n, const int32_t* __restrict__ indptr,
                            const int32_t* __restrict__ indices, const double* __restrict__ val,
@@ -438,11 +435,18 @@ __global__ void __launch_bounds__(SpmmLay<KP>::NT, 2)
   // tiles per step: narrow batches move few bytes per gather, so a row group keeps
   // two rows' gathers in flight (the rows are still summed in tile order)
   constexpr int UT = (KP <= 16) ? 2 : 1;
+  // how a row's 8 slots reach its lanes: at kp = 64 every lane reads them itself (L1
+  // broadcast, prefetched a step ahead), narrower batches stage them through shared
+  // memory (A/B timed: DESIGN.md §3.1)
+  constexpr bool SLOT_LDG = (KP >= 64);
   __shared__ double sm[M::RED];
   __shared__ double tot[KP];
   __shared__ int s_act[KP];
-  __shared__ __align__(16) int s_ci[2][UT][TR][ELL_W];
-  __shared__ __align__(16) double s_cv[2][UT][TR][ELL_W];
+  constexpr int SLOTS = SLOT_LDG ? 1 : 2 * UT * TR;  // shared slot staging (unused at kp = 64)
+  __shared__ __align__(16) int s_ci_[SLOTS][ELL_W];
+  __shared__ __align__(16) double s_cv_[SLOTS][ELL_W];
+  auto s_ci = reinterpret_cast<int(*)[UT][TR][ELL_W]>(&s_ci_[0][0]);
+  auto s_cv = reinterpret_cast<double(*)[UT][TR][ELL_W]>(&s_cv_[0][0]);
   if (MODE == MODE_PQ && c.summary[SUM_RUN] == 0) return;
   if (MODE == MODE_RESID && c.summary[SUM_CHECK] == 0) {
     if (blockIdx.x == 0 && threadIdx.x == 0) c.summary[SUM_REPLACE] = 0;
@@ -487,7 +491,7 @@ __global__ void __launch_bounds__(SpmmLay<KP>::NT, 2)
 #pragma unroll
   for (int u = 0; u < UT; ++u) {
     row[u] = tile_row(blockIdx.x + u * c.G);
-    if (!HF_SLOT_LDG) load_slots(row[u], ci[u], cv[u]);
+    if (!SLOT_LDG) load_slots(row[u], ci[u], cv[u]);
   }
   int b = 0;
   for (int t = blockIdx.x; t < nt; t += UT * c.G, b ^= 1) {
@@ -496,43 +500,40 @@ __global__ void __launch_bounds__(SpmmLay<KP>::NT, 2)
 #pragma unroll
     for (int u = 0; u < UT; ++u) {  // next step's slots in flight during this one
       rowN[u] = tile_row(t + (UT + u) * c.G);
-      if (!HF_SLOT_LDG) load_slots(rowN[u], ciN[u], cvN[u]);
+      if (!SLOT_LDG) load_slots(rowN[u], ciN[u], cvN[u]);
     }
-#if HF_SLOT_LDG
-    // every lane reads its row's 8 slots itself (L1 broadcast, one line per two rows),
-    // the next tile's rows prefetched into L1 one step ahead
-    if (gl == 0) {
+    if constexpr (SLOT_LDG) {
+      // every lane reads its row's 8 slots itself (L1 broadcast, one line per two rows),
+      // the next tile's rows prefetched into L1 one step ahead
+      if (gl == 0) {
 #pragma unroll
-      for (int u = 0; u < UT; ++u)
-        if (rowN[u] >= 0) {
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(A.ci + (size_t)rowN[u] * ELL_W));
-          asm volatile("prefetch.global.L1 [%0];" ::"l"(A.cv + (size_t)rowN[u] * ELL_W));
-        }
+        for (int u = 0; u < UT; ++u)
+          if (rowN[u] >= 0) {
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(A.ci + (size_t)rowN[u] * ELL_W));
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(A.cv + (size_t)rowN[u] * ELL_W));
+          }
+      }
+    } else {
+      if (gl < ELL_W) {
+#pragma unroll
+        for (int u = 0; u < UT; ++u)
+#pragma unroll
+          for (int k = 0; k < SPL; ++k) {
+            s_ci[b][u][grp][gl + k * LPR] = ci[u][k];
+            s_cv[b][u][grp][gl + k * LPR] = cv[u][k];
+          }
+      }
+      __syncwarp();
     }
-#else
-    if (gl < ELL_W) {
-#pragma unroll
-      for (int u = 0; u < UT; ++u)
-#pragma unroll
-        for (int k = 0; k < SPL; ++k) {
-          s_ci[b][u][grp][gl + k * LPR] = ci[u][k];
-          s_cv[b][u][grp][gl + k * LPR] = cv[u][k];
-        }
-    }
-    __syncwarp();
-#endif
     int cc[UT][ELL_W], c0x[UT];
     bool live[UT];
 #pragma unroll
     for (int u = 0; u < UT; ++u) {
-#if HF_SLOT_LDG
       const int rr = row[u] >= 0 ? row[u] : 0;
-      const int4 c0 = __ldg(reinterpret_cast<const int4*>(A.ci + (size_t)rr * ELL_W));
-      const int4 c1 = __ldg(reinterpret_cast<const int4*>(A.ci + (size_t)rr * ELL_W + 4));
-#else
-      const int4 c0 = *reinterpret_cast<const int4*>(&s_ci[b][u][grp][0]);
-      const int4 c1 = *reinterpret_cast<const int4*>(&s_ci[b][u][grp][4]);
-#endif
+      const int4 c0 = SLOT_LDG ? __ldg(reinterpret_cast<const int4*>(A.ci + (size_t)rr * ELL_W))
+                               : *reinterpret_cast<const int4*>(&s_ci[b][u][grp][0]);
+      const int4 c1 = SLOT_LDG ? __ldg(reinterpret_cast<const int4*>(A.ci + (size_t)rr * ELL_W + 4))
+                               : *reinterpret_cast<const int4*>(&s_ci[b][u][grp][4]);
       c0x[u] = c0.x;
       cc[u][0] = c0.x & (ELL_LONG - 1);
       cc[u][1] = c0.y;
@@ -575,19 +576,13 @@ __global__ void __launch_bounds__(SpmmLay<KP>::NT, 2)
 #pragma unroll
           for (int q = 0; q < CPL; ++q) g0[u][q] = g[u][0][q];
         }
-#if HF_SLOT_LDG
-        const double2* vp = reinterpret_cast<const double2*>(A.cv + (size_t)(row[u] >= 0 ? row[u] : 0) * ELL_W);
-#else
-        const double2* vp = reinterpret_cast<const double2*>(&s_cv[b][u][grp][0]);
-#endif
+        const double2* vp =
+            SLOT_LDG ? reinterpret_cast<const double2*>(A.cv + (size_t)(row[u] >= 0 ? row[u] : 0) * ELL_W)
+                     : reinterpret_cast<const double2*>(&s_cv[b][u][grp][0]);
         // consume the batch last-issued first (slot order 7..0)
 #pragma unroll
         for (int k2 = ELL_HB / 2 - 1; k2 >= 0; --k2) {
-#if HF_SLOT_LDG
-          const double2 vv = __ldg(vp + bt * ELL_HB / 2 + k2);
-#else
-          const double2 vv = vp[bt * ELL_HB / 2 + k2];
-#endif
+          const double2 vv = SLOT_LDG ? __ldg(vp + bt * ELL_HB / 2 + k2) : vp[bt * ELL_HB / 2 + k2];
 #pragma unroll
           for (int q = 0; q < CPL; ++q) a[u][q] = __fma_rn(vv.y, g[u][2 * k2 + 1][q], a[u][q]);
 #pragma unroll

@@ -144,3 +144,67 @@ def test_sharded_eit_leadfield_gloo(tmp_path, world):
     assert np.linalg.norm(got["m"] - ref) / np.linalg.norm(ref) <= 1e-6
     np.testing.assert_allclose(got["bg"], fx["eit_bg"], rtol=1e-8, atol=1e-14)
     assert int(got["p"]) == fx["eit_currents"].shape[1]
+
+
+def _fail_worker(rank, world, port, out):
+    """Rank 1 fails at its second column (global column 5); rank 0 converges."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_1811_07717_b200.distributed import sharded_leadfield
+    from paper_1811_07717_b200.engine import column_blocks
+    from paper_1811_07717_b200.errors import ConvergenceError
+
+    class FailingEngine:
+        L = 8
+
+        def __init__(self, cols):
+            self.c0, self.c1 = cols
+
+        def assemble(self):
+            return None
+
+        def solve(self, A):
+            if self.c0 == 4:
+                exc = ConvergenceError("no convergence", best_x=np.arange(6.0) + 0.5, residual=0.25,
+                                       iterations=17)
+                exc.local_column = 1
+                exc.column = self.c0 + 1
+                raise exc
+            return torch.zeros((6, self.c1 - self.c0), dtype=torch.float64)
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        eng = FailingEngine(column_blocks(8, world)[rank])
+        try:
+            sharded_leadfield(eng, world, rank)
+            np.save(out + f"{rank}.npy", np.array([-1.0]))
+        except ConvergenceError as exc:
+            np.save(out + f"{rank}.npy", np.concatenate([[exc.column, exc.residual, exc.iterations], exc.best_x]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_convergence_failure_raised_on_every_rank(tmp_path):
+    """One rank's ConvergenceError surfaces on every rank, with the global column and
+    the owner's best iterate, before any further collective (no rank hangs)."""
+    out = str(tmp_path / "e")
+    mp.spawn(_fail_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    for r in range(2):
+        got = np.load(out + f"{r}.npy")
+        np.testing.assert_array_equal(got, np.concatenate([[5.0, 0.25, 17.0], np.arange(6.0) + 0.5]))
+
+
+def test_helmet_306_geometry():
+    from paper_1811_07717_b200 import meg
+
+    s = meg.helmet_306()
+    assert s.n_sensors == 306 and s.kinds.count("mag") == 102
+    assert s.kinds.count("grad1") == s.kinds.count("grad2") == 102
+    np.testing.assert_allclose(np.linalg.norm(s.coils[:, 3:6], axis=1), 1.0)
+    assert np.all(s.coils[:, 2] >= -0.02 - 1e-12)  # the cap
+    grads = [i for i, k in enumerate(s.kinds) if k != "mag"]
+    for i in grads:  # a planar gradiometer: two coils, opposite weights, 16.8 mm apart
+        a, b = s.coil_ptr[i], s.coil_ptr[i + 1]
+        assert b - a == 2 and s.coils[a, 6] == -s.coils[a + 1, 6]
+        assert abs(np.linalg.norm(s.coils[a, :3] - s.coils[a + 1, :3]) - 0.0168) < 1e-12
