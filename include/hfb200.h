@@ -116,16 +116,20 @@ int hf_csr_prune_fill(const hf_csr* A, void* ws, size_t ws_bytes, int32_t* indpt
                       int32_t* indices_out, double* val_out, void* stream);
 
 /* Multi-RHS LDP-PCG: kp independent column recurrences of solver.py:64-111
- * advanced together through one CSR SpMM per iteration.
+ * advanced together through one SpMM per iteration.
  *   B, X       device, n x kp row-major (column j of the reference = X[:, j]);
- *              kp in {2,4,8,16,32,64,128}; unused columns must be zero in B.
+ *              kp in {2,4,8,16,32,64}; unused columns must be zero in B.
+ *              A column's result does not depend on kp or on the other columns
+ *              (canonical reductions: every dot product is summed in one order
+ *              that depends on n only), so T is bit-identical however the
+ *              columns are batched or sharded over ranks.
  *   d          device, n (LDP diagonal, or ones for preconditioner="none")
  *   freeze_at  device, kp int32, or NULL.  If given, column j stops right after
  *              iteration freeze_at[j] (freeze_at[j] < 0: run normally) — used to
  *              replay a failed column to its best iterate.
  *   iters, status, best_iter  host, kp int32 each
  *   true_res, best_res        host, kp double each
- * Workspace: hf_pcg_workspace_bytes(n, kp, A->nnz) bytes.
+ * Workspace: hf_pcg_workspace_bytes(n, kp, A->nnz) bytes.  n, nnz < 2^30.
  * Result per column: status HF_COL_*; iters = converged iteration count;
  * true_res = ||b - A x|| / ||b|| at exit; best_res/best_iter = smallest
  * recurrence residual seen and the iteration it occurred at. */
@@ -138,9 +142,8 @@ int hf_pcg_multi(const hf_csr* A, const double* d, const double* B, int32_t n, i
 /* Timing probe for the roofline report: runs `rounds` PCG rounds of the same
  * kernels as hf_pcg_multi (tolerance 0, so no column stops) and writes the
  * average duration in ms, measured with CUDA events on `stream`, of
- * {SpMM, k_update_r, k_update_xp} or, when bit 0 of *fused (host int32) is
- * set, of {k_xs, k_update_r, 0} (k_xs = x/p update fused with the next SpMM).
- * Bit 1 set: the SpMM is k_spmm_ell (ELL copy), else k_spmm_pq (CSR).
+ * {SpMM, r update, p update / x round averaged over the ring} to ms3;
+ * *flags (host int32) = 6 | (XD << 8), XD = the x-deferral depth.
  * Same workspace as hf_pcg_multi. */
 int hf_pcg_profile(const hf_csr* A, const double* d, const double* B, int32_t n, int32_t kp,
                    int32_t rounds, double* X, float* ms3, int32_t* fused, void* ws,

@@ -151,7 +151,7 @@ constexpr int ES_EC = 16;             // elements per chunk -> K = 64 per chunk 
 constexpr int ES_K = 4 * ES_EC;
 constexpr int ES_MAXP = 32, ES_MAXL = 64;  // patterns x electrode columns per CTA
 constexpr int ES_WARPS = ES_THREADS / 32;
-constexpr int ES_MAXT = (ES_MAXP / 8) * (ES_MAXL / 8) / ES_WARPS;  // output tiles per warp
+static_assert(ES_MAXP == 32 && ES_MAXL == 64 && ES_WARPS == 8, "8 warps x 16x16 blocks = 32 x 64");
 
 __host__ __device__ inline int es_stride(int w) { return ((w + 7) / 8) * 8 + ((((w + 7) / 8) * 8) % 16 == 0 ? 4 : 12); }
 
@@ -190,14 +190,14 @@ __global__ void __launch_bounds__(ES_THREADS, 3)
   __shared__ int32_t sC[2][ES_K];       // corner nodes of this chunk and the next
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, t4 = lane & 3;
-  const int MT = (np_ + 7) / 8, NTt = (nl + 7) / 8, ntile = MT * NTt;
+  const int wm = warp & 1, wn = warp >> 1;  // this warp's 16 x 16 output block
   // gather layout: 4 threads per chunk corner k = tid / 4; thread gq of a corner owns
   // columns gq, gq + 4, ... so a warp's accesses are 8 corners x 4 consecutive
   // doubles: one sector per corner in global memory, conflict-free in shared memory
   const int gk = tid >> 2, gq = tid & 3;
-  double acc[ES_MAXT][2];
+  double acc[4][2];  // tiles (rows +0/+8, columns +0/+8) of the warp's block
 #pragma unroll
-  for (int j = 0; j < ES_MAXT; ++j) acc[j][0] = acc[j][1] = 0.0;
+  for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = 0.0;
   const int e0 = dof_ptr[m], e1 = dof_ptr[m + 1];
   auto load_conn = [&](int eb, int buf) {
     if (tid < ES_K) {
@@ -252,26 +252,24 @@ __global__ void __launch_bounds__(ES_THREADS, 3)
       }
     }
     __syncthreads();
-    // 5) Q tiles += S' Tg on the fp64 tensor pipe; the warp's tiles advance together
-    //    through k so their DMMA chains overlap
-#pragma unroll 2
+    // 5) Q tiles += S' Tg on the fp64 tensor pipe.  Warp w owns the 2 x 2 block of
+    //    8x8 output tiles (rows 16 (w % 2) .., columns 16 (w / 2) ..): per k-step two A
+    //    and two B fragments feed four DMMAs, whose chains advance together.
+#pragma unroll 4
     for (int k0 = 0; k0 < ES_K; k0 += 4) {
-      const double* ar = sS + (size_t)(k0 + t4) * SP + g;  // A[row p][k] = S[k][p]
-      const double* br = sT + (size_t)(k0 + t4) * SL + g;  // B[k][col l] = Tg[k][l]
-#pragma unroll
-      for (int j = 0; j < ES_MAXT; ++j) {
-        const int ti = warp + ES_WARPS * j;
-        if (ti < ntile) dmma_8x8x4(acc[j][0], acc[j][1], ar[(ti % MT) * 8], br[(ti / MT) * 8]);
-      }
+      const double* ar = sS + (size_t)(k0 + t4) * SP + wm * 16 + g;  // A[row p][k] = S[k][p]
+      const double* br = sT + (size_t)(k0 + t4) * SL + wn * 16 + g;  // B[k][col l] = Tg[k][l]
+      const double a0 = ar[0], a1 = ar[8], b0 = br[0], b1 = br[8];
+      dmma_8x8x4(acc[0][0], acc[0][1], a0, b0);
+      dmma_8x8x4(acc[1][0], acc[1][1], a1, b0);
+      dmma_8x8x4(acc[2][0], acc[2][1], a0, b1);
+      dmma_8x8x4(acc[3][0], acc[3][1], a1, b1);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int j = 0; j < ES_MAXT; ++j) {
-    const int ti = warp + ES_WARPS * j;
-    if (ti >= ntile) break;
-    const int mt = ti % MT, nt = ti / MT;
-    const int p = mt * 8 + g, l = nt * 8 + 2 * t4;
+  for (int j = 0; j < 4; ++j) {
+    const int p = wm * 16 + (j & 1) * 8 + g, l = wn * 16 + (j >> 1) * 8 + 2 * t4;
     if (p < np_) {
       double* q = Q + ((size_t)(p0 + p) * n_dofs + m) * L + l0;
       if (l < nl) q[l] = acc[j][0];
