@@ -367,18 +367,15 @@ __global__ void __launch_bounds__(Map<KP>::NT)
 
 // ---------------------------------------------------------------- SpMM over an ELL copy
 // The SpMM runs on a padded ELL copy of the zero-free matrix (8 slots per row,
-// built once per solve by k_ell_fill) whose first three slots are positional:
-//   slot 0  the diagonal a_ii            (value only: its column is i)
-//   slot 1  a_i,i-1 (0.0 if absent)      (column i-1, clamped to a valid row)
-//   slot 2  a_i,i+1 (0.0 if absent)      (column i+1, clamped)
-//   slots 3..7  the row's other entries in CSR order; empty slots 3-4 hold
-//           (i, 0.0) and are gathered unconditionally (an exact zero, an L1 hit),
-//           empty slots 5-7 hold -1 and are skipped (an interior Kuhn row fills 3-6).
-// Slot 0's column field carries, for rows with more than 5 other entries, bit 30
-// and the CSR position of the first entry not held; the kernel reads those from
-// the CSR, skipping columns i-1..i+1.  Sum order, for every kp: slots 7..0, then
-// the CSR tail in order.  The x-neighbour slots are positional so a row group
-// can take p_{i-1}, p_i, p_{i+1} from rows it already holds (k_spmm_pair).
+// built once per solve by k_ell_fill).  Empty slots 0..ELL_OPT-1 hold (row
+// itself, 0.0): their gather hits L1 (the row's own p) and their FMA adds an
+// exact zero, so they are gathered and multiplied unconditionally; empty slots
+// from ELL_OPT on hold -1 and are skipped (an interior Kuhn row fills 7).  The
+// diagonal sits in slot 0, so the epilogue's p_i is its gather.  Rows with
+// more than 8 entries keep entries 0..7 in the slots and flag bit 30 of slot
+// 0's column; their entries 8.. come from the CSR.  Sum order, for every kp:
+// slots 7..0, then entries 8.. in order.  A/B timings of the variants are in
+// DESIGN.md §3.
 constexpr int ELL_LONG = 1 << 30;
 constexpr int ELL_OPT = 5;  // first slot gathered only when it holds an entry
 constexpr int ELL_HB = 4;   // gathers in flight per batch
@@ -388,35 +385,28 @@ __global__ void k_ell_fill(int n, const int32_t* __restrict__ indptr,
                            int* __restrict__ eci, double* __restrict__ ecv) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
+  const int st = indptr[i], ln = indptr[i + 1] - st;
   int c[ELL_W];
   double v[ELL_W];
-#pragma unroll
   for (int e = 0; e < ELL_W; ++e) {
-    c[e] = (e < ELL_OPT) ? i : -1;
+    c[e] = e >= ELL_OPT ? -1 : i;
     v[e] = 0.0;
-  }
-  int k = 3, tail = -1;
-  for (int j = indptr[i]; j < indptr[i + 1]; ++j) {
-    const int col = indices[j];
-    const double a = val[j];
-    if (col == i) {
-      v[0] = a;
-    } else if (col == i - 1) {
-      v[1] = a;
-    } else if (col == i + 1) {
-      v[2] = a;
-    } else if (k < ELL_W) {
-      c[k] = col;
-      v[k] = a;
-      ++k;
-    } else if (tail < 0) {
-      tail = j;
+    if (e < ln) {
+      c[e] = indices[st + e];
+      v[e] = val[st + e];
     }
   }
-  c[0] = tail >= 0 ? (ELL_LONG | tail) : 0;
-  c[1] = i > 0 ? i - 1 : i;
-  c[2] = i + 1 < n ? i + 1 : i;
-#pragma unroll
+  for (int e = 1; e < ELL_W && e < ln; ++e)  // the diagonal (when slot-held) to slot 0
+    if (c[e] == i) {
+      const int tc = c[0];
+      const double tv = v[0];
+      c[0] = c[e];
+      v[0] = v[e];
+      c[e] = tc;
+      v[e] = tv;
+      break;
+    }
+  if (ln > ELL_W) c[0] |= ELL_LONG;
   for (int e = 0; e < ELL_W; ++e) {
     eci[(size_t)i * ELL_W + e] = c[e];
     ecv[(size_t)i * ELL_W + e] = v[e];
@@ -545,7 +535,7 @@ __global__ void __launch_bounds__(SpmmLay<KP>::NT, 2)
       const int4 c1 = SLOT_LDG ? __ldg(reinterpret_cast<const int4*>(A.ci + (size_t)rr * ELL_W + 4))
                                : *reinterpret_cast<const int4*>(&s_ci[b][u][grp][4]);
       c0x[u] = c0.x;
-      cc[u][0] = rr;  // slot 0 is the diagonal (its column field holds the long-row tail)
+      cc[u][0] = c0.x & (ELL_LONG - 1);
       cc[u][1] = c0.y;
       cc[u][2] = c0.z;
       cc[u][3] = c0.w;
@@ -605,11 +595,10 @@ __global__ void __launch_bounds__(SpmmLay<KP>::NT, 2)
     for (int u = 0; u < UT; ++u) {  // epilogues in tile order (the canonical dot order)
       if (!live[u]) continue;
       const int r = row[u];
-      if (c0x[u] & ELL_LONG) {  // the CSR tail of a long row, in order, minus columns r-1..r+1
-        const int en = __ldg(A.indptr + r + 1);
-        for (int j = c0x[u] & (ELL_LONG - 1); j < en; ++j) {
+      if (c0x[u] & ELL_LONG) {  // entries 8.. of a long row, in order
+        const int st = __ldg(A.indptr + r), en = __ldg(A.indptr + r + 1);
+        for (int j = st + ELL_W; j < en; ++j) {
           const int ce = __ldg(A.indices + j);
-          if (ce >= r - 1 && ce <= r + 1) continue;
           const double ve = __ldg(A.val + j);
           double q2[CPL];
           ldg_cols<CPL>(Vl + (size_t)ce * KP, q2);
@@ -620,8 +609,15 @@ __global__ void __launch_bounds__(SpmmLay<KP>::NT, 2)
       const size_t o = (size_t)r * KP + gl * CPL;
       if constexpr (MODE == MODE_PQ) {
         st_cols<CPL>(Q + o, a[u]);
+        double pr[CPL];
+        if (cc[u][0] == r) {
 #pragma unroll
-        for (int q = 0; q < CPL; ++q) v[0][q] = __fma_rn(__dmul_rn(g0[u][q], a[u][q]), m[q], v[0][q]);
+          for (int q = 0; q < CPL; ++q) pr[q] = g0[u][q];
+        } else {
+          ldg_cols<CPL>(V + o, pr);
+        }
+#pragma unroll
+        for (int q = 0; q < CPL; ++q) v[0][q] = __fma_rn(__dmul_rn(pr[q], a[u][q]), m[q], v[0][q]);
       } else {
         double bb[CPL], sres[CPL];
         ld_cols<CPL>(Bv + o, bb);
@@ -668,166 +664,6 @@ __global__ void __launch_bounds__(SpmmLay<KP>::NT, 2)
     census<KP>(c, st);
     if (tid == 0) c.summary[SUM_REPLACE] = nrep;
   }
-}
-
-// q = A p at kp = 64 with row pairs (MODE_PQ): a row group of 16 lanes (4 columns
-// each) owns rows r = 32 t + 2 h and r + 1 of every tile and loads p_{r-1} .. p_{r+2}
-// once — the diagonal and x-neighbour slots (0-2, positional) of both rows come
-// from those four rows, so only slots 3-7 are gathered: 12 row loads per pair
-// instead of 14-16.  Same entries, same order (slots 7..0, then the CSR tail),
-// so q is bitwise k_spmm's.  The pair's two rows keep separate p.q accumulators,
-// added at the end: the first level of the balanced row-group tree, so the
-// canonical reduction order is unchanged.
-struct PairLay {
-  static constexpr int KP = 64, CPL = 4, LPR = 16;
-  static constexpr int NT = (TR / 2) * LPR;  // 256 threads: 16 row pairs
-  static constexpr int NW = NT / 32;
-  static constexpr int RED = (NW * KP * 2 > RSEG * KP * 2) ? NW * KP * 2 : RSEG * KP * 2;
-};
-
-__global__ void __launch_bounds__(PairLay::NT, 2)
-    k_spmm_pair(Ctl c, Ell A, const double* __restrict__ V, double* __restrict__ Q) {
-  using M = PairLay;
-  constexpr int KP = M::KP, CPL = M::CPL, LPR = M::LPR;
-  __shared__ double sm[M::RED];
-  __shared__ double tot[KP];
-  __shared__ int s_act[KP];
-  if (c.summary[SUM_RUN] == 0) return;
-  const int tid = threadIdx.x, gl = tid % LPR, h = tid / LPR;
-  for (int j = tid; j < KP; j += M::NT) s_act[j] = (c.state[j] == S_RUN);
-  __syncthreads();
-  double m[CPL];
-  bool any = false;
-#pragma unroll
-  for (int k = 0; k < CPL; ++k) {
-    const bool a = s_act[gl * CPL + k] != 0;
-    m[k] = a ? 1.0 : 0.0;
-    any |= a;
-  }
-  const int n = c.n, nt = n_tiles(n);
-  const double* __restrict__ Vl = V + gl * CPL;
-  double v0[CPL], v1[CPL];  // p.q of the pair's even and odd rows
-#pragma unroll
-  for (int k = 0; k < CPL; ++k) v0[k] = v1[k] = 0.0;
-  for (int t = blockIdx.x; t < nt; t += c.G) {
-    const int r = t * TR + 2 * h;
-    if (gl == 0) {  // the next tile's slot rows into L1
-      const int rn = r + c.G * TR;
-      if (rn < n) {
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(A.ci + (size_t)rn * ELL_W));
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(A.cv + (size_t)rn * ELL_W));
-      }
-    }
-    if (r >= n || !any) continue;
-    const bool two = r + 1 < n;
-    const int r1 = two ? r + 1 : r;
-    // p_{r-1}, p_r, p_{r+1}, p_{r+2} (clamped: a clamped row only meets a 0.0 slot)
-    double x[4][CPL];
-    ldg_cols<CPL>(Vl + (size_t)(r > 0 ? r - 1 : r) * KP, x[0]);
-    ldg_cols<CPL>(Vl + (size_t)r * KP, x[1]);
-    ldg_cols<CPL>(Vl + (size_t)(r + 1 < n ? r + 1 : r) * KP, x[2]);
-    ldg_cols<CPL>(Vl + (size_t)(r + 2 < n ? r + 2 : r1) * KP, x[3]);
-    const int4 ca0 = __ldg(reinterpret_cast<const int4*>(A.ci + (size_t)r * ELL_W));
-    const int4 ca1 = __ldg(reinterpret_cast<const int4*>(A.ci + (size_t)r * ELL_W + 4));
-    const int4 cb0 = __ldg(reinterpret_cast<const int4*>(A.ci + (size_t)r1 * ELL_W));
-    const int4 cb1 = __ldg(reinterpret_cast<const int4*>(A.ci + (size_t)r1 * ELL_W + 4));
-    const int ca[5] = {ca0.w, ca1.x, ca1.y, ca1.z, ca1.w};  // slots 3..7
-    const int cb[5] = {cb0.w, cb1.x, cb1.y, cb1.z, cb1.w};
-    const double2* va = reinterpret_cast<const double2*>(A.cv + (size_t)r * ELL_W);
-    const double2* vb = reinterpret_cast<const double2*>(A.cv + (size_t)r1 * ELL_W);
-    double aa[CPL], ab[CPL];
-#pragma unroll
-    for (int q = 0; q < CPL; ++q) aa[q] = ab[q] = 0.0;
-    {  // slots 7, 6, 5 (gathered only when filled) and 4, 3 (an empty one holds (row, 0.0))
-      double ga[5][CPL], gb[5][CPL];
-#pragma unroll
-      for (int e = 4; e >= 0; --e) {  // slot 3 + e
-#pragma unroll
-        for (int q = 0; q < CPL; ++q) ga[e][q] = gb[e][q] = 0.0;
-        if (e >= ELL_OPT - 3) {
-          if (ca[e] >= 0) ldg_cols<CPL>(Vl + (size_t)ca[e] * KP, ga[e]);
-          if (cb[e] >= 0) ldg_cols<CPL>(Vl + (size_t)cb[e] * KP, gb[e]);
-        } else {
-          if (ca[e] != r) ldg_cols<CPL>(Vl + (size_t)ca[e] * KP, ga[e]);
-          else {
-#pragma unroll
-            for (int q = 0; q < CPL; ++q) ga[e][q] = x[1][q];
-          }
-          if (cb[e] != r1) ldg_cols<CPL>(Vl + (size_t)cb[e] * KP, gb[e]);
-          else {
-#pragma unroll
-            for (int q = 0; q < CPL; ++q) gb[e][q] = x[2][q];
-          }
-        }
-      }
-      // slot order 7..3 (values in pairs: slots 2k, 2k+1 share a double2)
-      const double2 a76 = __ldg(va + 3), b76 = __ldg(vb + 3);
-      const double2 a54 = __ldg(va + 2), b54 = __ldg(vb + 2);
-      const double2 a32 = __ldg(va + 1), b32 = __ldg(vb + 1);
-#pragma unroll
-      for (int q = 0; q < CPL; ++q) {
-        aa[q] = __fma_rn(a76.y, ga[4][q], aa[q]);
-        aa[q] = __fma_rn(a76.x, ga[3][q], aa[q]);
-        aa[q] = __fma_rn(a54.y, ga[2][q], aa[q]);
-        aa[q] = __fma_rn(a54.x, ga[1][q], aa[q]);
-        aa[q] = __fma_rn(a32.y, ga[0][q], aa[q]);
-        ab[q] = __fma_rn(b76.y, gb[4][q], ab[q]);
-        ab[q] = __fma_rn(b76.x, gb[3][q], ab[q]);
-        ab[q] = __fma_rn(b54.y, gb[2][q], ab[q]);
-        ab[q] = __fma_rn(b54.x, gb[1][q], ab[q]);
-        ab[q] = __fma_rn(b32.y, gb[0][q], ab[q]);
-      }
-      // slots 2, 1, 0: x-neighbours and the diagonal from the held rows
-      const double2 a10 = __ldg(va), b10 = __ldg(vb);
-#pragma unroll
-      for (int q = 0; q < CPL; ++q) {
-        aa[q] = __fma_rn(a32.x, x[2][q], aa[q]);
-        aa[q] = __fma_rn(a10.y, x[0][q], aa[q]);
-        aa[q] = __fma_rn(a10.x, x[1][q], aa[q]);
-        ab[q] = __fma_rn(b32.x, x[3][q], ab[q]);
-        ab[q] = __fma_rn(b10.y, x[1][q], ab[q]);
-        ab[q] = __fma_rn(b10.x, x[2][q], ab[q]);
-      }
-    }
-    if (ca0.x & ELL_LONG) {  // CSR tails, in order, minus columns r-1..r+1
-      const int en = __ldg(A.indptr + r + 1);
-      for (int j = ca0.x & (ELL_LONG - 1); j < en; ++j) {
-        const int ce = __ldg(A.indices + j);
-        if (ce >= r - 1 && ce <= r + 1) continue;
-        const double ve = __ldg(A.val + j);
-        double q2[CPL];
-        ldg_cols<CPL>(Vl + (size_t)ce * KP, q2);
-#pragma unroll
-        for (int q = 0; q < CPL; ++q) aa[q] = __fma_rn(ve, q2[q], aa[q]);
-      }
-    }
-    if (two && (cb0.x & ELL_LONG)) {
-      const int en = __ldg(A.indptr + r1 + 1);
-      for (int j = cb0.x & (ELL_LONG - 1); j < en; ++j) {
-        const int ce = __ldg(A.indices + j);
-        if (ce >= r1 - 1 && ce <= r1 + 1) continue;
-        const double ve = __ldg(A.val + j);
-        double q2[CPL];
-        ldg_cols<CPL>(Vl + (size_t)ce * KP, q2);
-#pragma unroll
-        for (int q = 0; q < CPL; ++q) ab[q] = __fma_rn(ve, q2[q], ab[q]);
-      }
-    }
-    st_cols<CPL>(Q + (size_t)r * KP + gl * CPL, aa);
-#pragma unroll
-    for (int q = 0; q < CPL; ++q) v0[q] = __fma_rn(__dmul_rn(x[1][q], aa[q]), m[q], v0[q]);
-    if (two) {
-      st_cols<CPL>(Q + (size_t)r1 * KP + gl * CPL, ab);
-#pragma unroll
-      for (int q = 0; q < CPL; ++q) v1[q] = __fma_rn(__dmul_rn(x[2][q], ab[q]), m[q], v1[q]);
-    }
-  }
-  double v[1][CPL];
-#pragma unroll
-  for (int q = 0; q < CPL; ++q) v[0][q] = __dadd_rn(v0[q], v1[q]);  // tree level 0: rows 2h, 2h+1
-  block_partials<M, 1>(v, sm, c);
-  if (!last_block_reduce<M, 1>(c, sm, tot)) return;
-  if (tid < KP && s_act[tid]) c.alpha[tid] = c.rz[tid] / tot[tid];
 }
 
 // r -= alpha q ; res = |r|/|b| ; best ; tolerance / max_iter ; beta   (solver.py:90-106)
@@ -1294,10 +1130,7 @@ inline void launch_round(const Grids& g0, const Layout& L, double* X, int r, cud
     k->xmask = L.xmask + (size_t)slot * KP;
   }
   double* Pc = L.P + (size_t)slot * nk;
-  if constexpr (KP == 64)
-    k_spmm_pair<<<g.c.G, PairLay::NT, 0, q>>>(g.c, g.ell, Pc, L.Q);
-  else
-    k_spmm<KP, MODE_PQ><<<g.c.G, SpmmLay<KP>::NT, 0, q>>>(g.c, g.ell, Pc, nullptr, L.Q);
+  k_spmm<KP, MODE_PQ><<<g.c.G, SpmmLay<KP>::NT, 0, q>>>(g.c, g.ell, Pc, nullptr, L.Q);
   if (ev) cudaEventRecord(ev[1], q);
   k_update_r<KP><<<g.c.G, M::NT, 0, q>>>(g.c, L.Q, L.R);
   if (ev) cudaEventRecord(ev[2], q);
@@ -1552,8 +1385,8 @@ extern "C" int hf_pcg_multi(const hf_csr* A, const double* d, const double* B, i
               A->n_rows, A->n_cols, max_iter);
     return HF_ERR_ARG;
   }
-  if (n >= (1 << 30) || A->nnz >= (1LL << 30)) {
-    set_error("hf_pcg_multi: n=%d / nnz=%lld exceed the ELL index range", n, (long long)A->nnz);
+  if (n >= (1 << 30)) {
+    set_error("hf_pcg_multi: n=%d exceeds the ELL column range", n);
     return HF_ERR_ARG;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
