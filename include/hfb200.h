@@ -129,7 +129,7 @@ int hf_csr_prune_fill(const hf_csr* A, void* ws, size_t ws_bytes, int32_t* indpt
  *              replay a failed column to its best iterate.
  *   iters, status, best_iter  host, kp int32 each
  *   true_res, best_res        host, kp double each
- * Workspace: hf_pcg_workspace_bytes(n, kp, A->nnz) bytes.  n, nnz < 2^30.
+ * Workspace: hf_pcg_workspace_bytes(n, kp, A->nnz) bytes.  n < 2^30.
  * Result per column: status HF_COL_*; iters = converged iteration count;
  * true_res = ||b - A x|| / ||b|| at exit; best_res/best_iter = smallest
  * recurrence residual seen and the iteration it occurred at. */
