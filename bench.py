@@ -393,6 +393,61 @@ def run_meg(args):
     print(json.dumps(out), flush=True)
 
 
+def run_eit(args):
+    """C4 (BASELINE.json configs[3]): the linearised EIT lead field on the C2 mesh,
+    64 electrodes, 32 adjacent-pair patterns, 5,000 conductivity DOFs.  One step =
+    eit_leadfield (leadfield.py:210-237): 64 transfer solves, 32 pattern solves, the
+    DMMA sensitivities and the 2,048 x 5,000 Jacobian; RHS-solves/s counts both
+    kinds of solves (96 per step)."""
+    import torch
+
+    from paper_1811_07717_b200 import _native as N
+    from paper_1811_07717_b200 import model, synthetic
+    from paper_1811_07717_b200.fem import assemble_A
+    from paper_1811_07717_b200.leadfield import adjacent_pair_patterns, build_dof_map, eit_leadfield
+    from paper_1811_07717_b200.solver import PcgConfig
+    from paper_1811_07717_b200.topology import electrodes_from_centers
+
+    torch.cuda.set_device(0)
+    cfg = PcgConfig(tolerance=1e-8)
+    mesh = synthetic.sphere_mesh(synthetic.C2_RADII, synthetic.C2_COND, 0.0015)
+    el = electrodes_from_centers(mesh, synthetic.fibonacci_sphere_points(64, 0.092), 0.012, 1e3)
+    t0 = time.perf_counter()
+    dofs = build_dof_map(mesh, [0, 1], 5000, seed=2)
+    t_dof = time.perf_counter() - t0
+    B, C, R = model.assemble_B_C_R(mesh, el)
+    sysm = model.CemSystem(mesh=mesh, electrodes=el, A=assemble_A(mesh, el), B=B, C=C, R=R,
+                           ground=model.ground_node(mesh, el))
+    I = adjacent_pair_patterns(64)[:, :32]
+    for _ in range(args.warmup):
+        eit_leadfield(sysm, dofs, I, cfg)
+    torch.cuda.synchronize()
+    launches0 = N.lib.hf_launch_count()
+    with ClockSampler(0) as clocks:
+        w0 = time.perf_counter()
+        for _ in range(args.steps):
+            lf = eit_leadfield(sysm, dofs, I, cfg)
+        torch.cuda.synchronize()
+        wall = (time.perf_counter() - w0) / args.steps
+    launches = N.lib.hf_launch_count() - launches0
+    solves = 64 + 32
+    out = {"metric": METRIC, "value": round(solves / wall, 3), "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": round(wall * 1e3, 2), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (C2 mesh, 64 fibonacci electrodes r = 12 mm, adjacent-pair patterns, "
+                   "volume-weighted DOF centres, seed 2)",
+           "config": {"workload": "c4: linearised EIT lead field on the 1,001,184-node C2 mesh, 64 electrodes, "
+                                  "32 injection patterns, 5,000 conductivity DOFs (4,105,824 DOF elements)",
+                      "config": "c4", "lf_shape": list(lf.matrix.shape), "tolerance": cfg.tolerance,
+                      "precision": "fp64", "parallelism": "columns x1"},
+           "e2e": {"value": round(solves / wall, 3), "unit": UNIT,
+                   "h2d_bytes_per_step": int(12 * sysm.A.nnz + 4 * (sysm.A.shape[0] + 1) + 20 * B.nnz),
+                   "d2h_bytes_per_step": int(lf.matrix.nbytes),
+                   "api": "eit_leadfield(sys, dofs, currents) with host scipy A/B (the drop-in signature)"},
+           "build_dof_map_s": round(t_dof, 3), "gpu_launches": int(launches), "clocks": clocks.summary()}
+    print(json.dumps(out), flush=True)
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -581,6 +636,10 @@ def run_reference(args):
     if args.config == "c3":
         print(json.dumps({"impl": "reference", "unavailable": "the reference has no MEG lead field (SPEC.md:8)"}))
         return
+    if args.config == "c4":
+        print(json.dumps({"impl": "reference", "unavailable": "C4's build_dof_map needs a 459 GiB array in the "
+                                                              "reference (leadfield.py:98)"}))
+        return
     import multiprocessing as mp
 
     hf = _import_reference()
@@ -637,7 +696,7 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=["c1", "c2", "c3", "c5"], default="c2")
+    ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5"], default="c2")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--ref-cores", type=int, default=0)
@@ -648,6 +707,8 @@ def main():
         run_reference(args)
     elif args.config == "c3":
         run_meg(args)
+    elif args.config == "c4":
+        run_eit(args)
     else:
         run_ours(args)
 
