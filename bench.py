@@ -172,7 +172,10 @@ def kernel_roofline(Bd, A, rounds=24, config="c2"):
     ach = kern[dominant]["gbs"]
     return {"bound": "hbm", "kernel": f"{dominant}<{kp}>", "achieved": round(ach, 1),
             "peak": peak, "peak_kind": peak_kind, "unit": "GB/s", "frac": round(ach / peak, 4),
-            "traffic": traffic, "algorithmic_bytes_per_launch": algo[dominant],
+            "traffic": traffic,
+            "traffic_source": "profiles/traffic.json: dram__bytes_read.sum + dram__bytes_write.sum per launch from "
+                              "one ncu --set full capture of these kernels (tools/refresh_profiles.sh ncu)",
+            "algorithmic_bytes_per_launch": algo[dominant],
             "launch_ms": round(times[dominant], 4),
             "share_of_round": round(times[dominant] / total_ms, 3),
             "pcg_round": {"kp": kp, "n": n, "nnz_spmm": nnz, "x_deferral": xd,
