@@ -194,3 +194,41 @@ def test_batch_width_policy():
     assert PcgOperator.batch_width(bw(35_031), 256, 64) == 32   # C5
     assert PcgOperator.batch_width(bw(10 ** 7), 256, 64) == 16  # floor
     assert PcgOperator.batch_width(bw(100), 5, 64) == 5
+
+
+def test_abi_rejects_bad_arguments_without_a_gpu():
+    """Argument validation happens before any CUDA call: every entry point returns
+    HF_ERR_ARG (1) with a message on null pointers / bad shapes / unsupported widths."""
+    import ctypes as C
+
+    from paper_1811_07717_b200 import _native as N
+
+    L = N.lib
+    P = None
+    arr = (C.c_int32 * 8)()
+    dbl = (C.c_double * 8)()
+    csr = N.HfCsr(10, 10, 30, 1, 1, 1)  # dummy (non-null) pointers
+    # hf_pcg_multi: null argument, bad shape, unsupported kp
+    assert L.hf_pcg_multi(None, P, P, 10, 4, 1e-8, 10, P, P, arr, arr, dbl, dbl, arr, P, 0, P) == 1
+    assert b"null argument" in L.hf_last_error()
+    rc = L.hf_pcg_multi(C.byref(csr), 1, 1, 11, 4, 1e-8, 10, P, 1, arr, arr, dbl, dbl, arr, 1, 0, P)
+    assert rc == 1 and b"bad shape" in L.hf_last_error()
+    rc = L.hf_pcg_multi(C.byref(csr), 1, 1, 10, 128, 1e-8, 10, P, 1, arr, arr, dbl, dbl, arr, 1, 0, P)
+    assert rc == 1 and b"kp=128" in L.hf_last_error()
+    rc = L.hf_pcg_multi(C.byref(csr), 1, 1, 10, 4, 0.0, 10, P, 1, arr, arr, dbl, dbl, arr, 1, 0, P)
+    assert rc == 1  # tol must be > 0 (PcgConfig's rule)
+    assert L.hf_ldp(None, P, P, None, P) == 1
+    assert L.hf_eit_sens(P, P, P, P, 1, 0, P, 4, 4, P, 4, 2, P, P, 0, P) == 1
+    assert L.hf_meg_rhs(P, P, P, 10, 10, 0, P, P, 600, P, 600, P, 0, P) == 1
+    assert L.hf_lf_tail(P, 4, 4, None, P, 4, 4, P, P) == 1
+    assert L.hf_ground_node(P, 0, P, 0, 10, P, None, P) == 1
+    assert L.hf_dof_partition(P, P, 10, 0, P, P, P, 0, P) == 1
+
+
+def test_abi_workspace_queries_cover_new_entry_points():
+    from paper_1811_07717_b200 import _native as N
+
+    assert N.lib.hf_eit_sens_workspace_bytes(4_105_824) >= 4_105_824 * 16 * 8
+    assert N.lib.hf_meg_workspace_bytes(1000, 5800) > 5800 * 16 * 8
+    assert N.lib.hf_ground_node_workspace_bytes(1000) >= 4 * 1002
+    assert N.lib.hf_dof_partition_workspace_bytes(100_000) > 100_000 * 4
