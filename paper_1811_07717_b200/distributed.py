@@ -75,32 +75,41 @@ def _all_gather_columns(X, blocks, group):
 
 
 def _solve_consistently(solve, c0, n_cols, blocks, group, tag):
-    """Run this rank's solve; if any rank's columns fail, every rank raises the same
-    ConvergenceError before the next collective (the reference's transfer_matrix
-    reports the first failing column in index order, solver.py:129-136): the
-    lowest failing global column wins, and its owner broadcasts best_x."""
+    """Run this rank's solve; if any rank's columns fail, every rank raises before the
+    next collective, so no rank is left waiting in it.  Convergence failures become
+    the same ConvergenceError on every rank (the reference's transfer_matrix reports
+    the first failing column in index order, solver.py:129-136): the lowest failing
+    global column wins and its owner broadcasts best_x, residual and iterations.
+    Any other exception is re-raised where it happened and reported as a
+    RuntimeError on the other ranks."""
     from .errors import ConvergenceError
 
-    err, X = None, None
+    err, other, X = None, None, None
     try:
         X = solve()
     except ConvergenceError as exc:
         err = exc
+    except Exception as exc:  # noqa: BLE001 - re-raised below, after the agreement
+        other = exc
     mine = n_cols if err is None else c0 + int(getattr(err, "local_column", 0))
-    first = mine
-    flag = torch.tensor([first], dtype=torch.int64)
+    flag = torch.tensor([mine, 1 if other is not None else 0], dtype=torch.int64)
     if not _host_collectives(group):
         flag = flag.cuda()
-    dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
-    first = int(flag.item())
+    first_t = flag[:1].clone()
+    any_other = flag[1:].clone()
+    dist.all_reduce(first_t, op=dist.ReduceOp.MIN, group=group)
+    dist.all_reduce(any_other, op=dist.ReduceOp.MAX, group=group)
+    if int(any_other.item()):
+        if other is not None:
+            raise other
+        raise RuntimeError("the sharded solve failed on another rank")
+    first = int(first_t.item())
     if first >= n_cols:
         return X
     owner = next(r for r, (b0, b1) in enumerate(blocks) if b0 <= first < b1)
     meta = torch.zeros(3, dtype=torch.float64)
-    n = None
     if err is not None and mine == first:
-        n = len(err.best_x)
-        meta[:] = torch.tensor([float(n), float(err.residual), float(err.iterations)])
+        meta[:] = torch.tensor([float(len(err.best_x)), float(err.residual), float(err.iterations)])
     if not _host_collectives(group):
         meta = meta.cuda()
     dist.broadcast(meta, src=_global_rank(owner, group), group=group)
@@ -111,8 +120,7 @@ def _solve_consistently(solve, c0, n_cols, blocks, group, tag):
     if not _host_collectives(group):
         best = best.cuda()
     dist.broadcast(best, src=_global_rank(owner, group), group=group)
-    out = ConvergenceError(str(err) if err is not None else
-                           f"PCG did not converge in column {first} (rank {owner})",
+    out = ConvergenceError(f"PCG did not converge in {iters} iterations (best residual {residual:.3e})",
                            best_x=best.cpu().numpy(), residual=residual, iterations=iters)
     if tag:
         out.column = first
