@@ -219,15 +219,31 @@ def response_matrix_device(dsys, T):
     return symmetrize(response_block_device(dsys.Bt, T, dsys.L, dsys.Cdiag).cpu().numpy())
 
 
+_BLAS = None
+
+
+def _one_blas_thread():
+    """A context that runs BLAS/LAPACK single-threaded: for an L x L (L <= 256)
+    factorisation a multi-threaded OpenBLAS spends 5-200 ms synchronising its
+    threads against well under 1 ms of work (measured on the GPU box and here)."""
+    global _BLAS
+    if _BLAS is None:
+        from threadpoolctl import ThreadpoolController
+
+        _BLAS = ThreadpoolController()
+    return _BLAS.limit(limits=1, user_api="blas")
+
+
 def _solve_response(M, rhs):
     """lu_factor / lu_solve with the reference's singularity rule (leadfield.py:112-119)."""
-    try:
-        lu, piv = sla.lu_factor(M)
-    except (ValueError, sla.LinAlgError) as exc:
-        raise SingularSystemError(f"electrode response factorization failed: {exc}")
-    if np.any(np.abs(np.diag(lu)) < 1e-300):
-        raise SingularSystemError("electrode response matrix is singular")
-    return sla.lu_solve((lu, piv), rhs)
+    with _one_blas_thread():
+        try:
+            lu, piv = sla.lu_factor(M)
+        except (ValueError, sla.LinAlgError) as exc:
+            raise SingularSystemError(f"electrode response factorization failed: {exc}")
+        if np.any(np.abs(np.diag(lu)) < 1e-300):
+            raise SingularSystemError("electrode response matrix is singular")
+        return sla.lu_solve((lu, piv), rhs)
 
 
 def _electrode_response_device(sys, cfg):
@@ -263,7 +279,9 @@ def lf_tail_device(T, Gt, W):
 def response_operator(M, R):
     """W = -R M^-1 (L x L) with the reference's LU (leadfield.py:112-119, 129)."""
     L = M.shape[0]
-    return -(R @ _solve_response(M, np.eye(L)))
+    X = _solve_response(M, np.eye(L))
+    with _one_blas_thread():
+        return -(R @ X)
 
 
 def eeg_leadfield(sys, cfg=PcgConfig(), threads=1):
