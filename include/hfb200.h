@@ -26,6 +26,7 @@
  *   hf_lf_tail             leadfield.py:122-134 eeg_leadfield: L = W (G'T)'  with W = -R M^-1
  *   hf_dense_lf            leadfield.py:230-237 eit_leadfield column blocks  W Q[p]'
  *   hf_eit_sens            leadfield.py:179-207 _dof_sensitivities: Q[p,m,:] = T' K_m u_p
+ *   hf_csr_dense           leadfield.py:223    eit_leadfield's pattern right-hand sides B V
  *   hf_boundary_faces      meshgen.py:101-134  TetMesh.boundary_triangles
  *   hf_whitney_gt          fem.py:291-422      assemble_G (Whitney source matrix), as G'
  *   hf_nearest_center      leadfield.py:96-99  build_dof_map: owner = argmin ||c_i - centre_j||
@@ -223,6 +224,11 @@ int hf_dense_lf(const double* Qc, int32_t ncols, int32_t K, const double* W, int
  *      bytes (the DOF elements' unit blocks)
  * The contraction runs on the fp64 tensor pipe (DMMA m8n8k4), one GEMM with
  * K = 4 |E_m| per DOF. */
+/* out (device n_rows x ldo row-major, ncols used) = A (CSR) D (device A->n_cols x ldd
+ * row-major): the EIT pattern right-hand sides B M^-1 I (leadfield.py:223). */
+int hf_csr_dense(const hf_csr* A, const double* D, int32_t ldd, int32_t ncols, double* out,
+                 int32_t ldo, void* stream);
+
 size_t hf_eit_sens_workspace_bytes(int64_t n_dof_elems);
 int hf_eit_sens(const double* nodes, const int32_t* tetra, const int32_t* dof_elems,
                 const int32_t* dof_ptr, int32_t n_dofs, int32_t ground, const double* T,

@@ -20,6 +20,7 @@ holds the comparison.
 from .solver import ConvergenceFailure, PcgSettings, ldp, pcg_solve, transfer_matrix
 from .fem import assemble_A, ground_node, stiffness_blocks, volume_stiffness
 from .leadfield import (
+    build_dof_map,
     dof_sensitivities,
     eeg_leadfield,
     eit_forward,
@@ -31,6 +32,6 @@ from .leadfield import (
 __all__ = [
     "ConvergenceFailure", "PcgSettings", "ldp", "pcg_solve", "transfer_matrix",
     "assemble_A", "ground_node", "stiffness_blocks", "volume_stiffness",
-    "dof_sensitivities", "eeg_leadfield", "eit_forward", "eit_leadfield",
+    "build_dof_map", "dof_sensitivities", "eeg_leadfield", "eit_forward", "eit_leadfield",
     "electrode_response", "solve_response",
 ]

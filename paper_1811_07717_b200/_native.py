@@ -59,6 +59,7 @@ def _load():
         "hf_lf_tail": (C.c_int, [P, I32, I32, pcsr, P, I32, I32, P, P]),
         "hf_dense_lf": (C.c_int, [P, I32, I32, P, I32, I32, P, I32, P]),
         "hf_eit_sens_workspace_bytes": (SZ, [I64]),
+        "hf_csr_dense": (C.c_int, [pcsr, P, I32, I32, P, I32, P]),
         "hf_eit_sens": (C.c_int, [P, P, P, P, I32, I32, P, I32, I32, P, I32, I32, P, P, SZ, P]),
         "hf_topology_workspace_bytes": (SZ, [I32, I32, I32]),
         "hf_boundary_faces": (C.c_int, [P, I32, I32, P, C.POINTER(I64), P, SZ, P]),
@@ -95,7 +96,7 @@ EXPORTED = ("hf_version", "hf_last_error", "hf_device_sm_count", "hf_launch_coun
             "hf_csr_prune_workspace_bytes", "hf_csr_prune_count", "hf_csr_prune_fill",
             "hf_pcg_workspace_bytes", "hf_pcg_multi", "hf_pcg_profile", "hf_p1_blocks",
             "hf_p1_assemble_workspace_bytes", "hf_p1_assemble_prepare", "hf_p1_assemble_fill",
-            "hf_response_matrix", "hf_lf_tail", "hf_dense_lf", "hf_eit_sens_workspace_bytes", "hf_eit_sens",
+            "hf_response_matrix", "hf_lf_tail", "hf_dense_lf", "hf_csr_dense", "hf_eit_sens_workspace_bytes", "hf_eit_sens",
             "hf_topology_workspace_bytes", "hf_boundary_faces", "hf_whitney_gt",
             "hf_nearest_center", "hf_triangle_centroids", "hf_tet_centroids",
             "hf_dof_partition_workspace_bytes", "hf_dof_partition", "hf_ground_node_workspace_bytes",

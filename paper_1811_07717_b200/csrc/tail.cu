@@ -27,6 +27,22 @@ __global__ void k_bt_t(int L, int col0, int ncols, const int32_t* __restrict__ p
   }
 }
 
+// ---------------------------------------------------------------- sparse x dense
+// out (n x ncols, row-major) = A (CSR n x k) D (k x ncols, row-major): the EIT
+// pattern right-hand sides B V (leadfield.py:223), rows summed in CSR order as
+// scipy's csr_matvecs does (a product, then an add).
+__global__ void k_csr_dense(int n, int ncols, const int32_t* __restrict__ ptr,
+                            const int32_t* __restrict__ idx, const double* __restrict__ val,
+                            const double* __restrict__ D, int ldd, double* __restrict__ out, int ldo) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (size_t)n * ncols) return;
+  const int i = (int)(t / ncols), c = (int)(t % ncols);
+  double acc = 0.0;
+  for (int q = ptr[i]; q < ptr[i + 1]; ++q)
+    acc = __dadd_rn(acc, __dmul_rn(val[q], D[(size_t)idx[q] * ldd + c]));
+  out[(size_t)i * ldo + c] = acc;
+}
+
 // ---------------------------------------------------------------- DMMA tile GEMM
 constexpr int LF_THREADS = 256;
 constexpr int LF_NC = 32;  // source columns per CTA
@@ -388,6 +404,22 @@ extern "C" int hf_eit_sens(const double* nodes, const int32_t* tetra, const int3
   dim3 grid(n_dofs, (L + tail::ES_MAXL - 1) / tail::ES_MAXL, (P + tail::ES_MAXP - 1) / tail::ES_MAXP);
   tail::k_eit_sens<<<grid, tail::ES_THREADS, smem, s>>>(Kbuf, tetra, dof_elems, dof_ptr, n_dofs, T,
                                                         ldt, L, U, ldu, P, Q);
+  HF_LAUNCH_CHECK();
+  count_launches(1);
+  return HF_OK;
+}
+
+extern "C" int hf_csr_dense(const hf_csr* A, const double* D, int32_t ldd, int32_t ncols, double* out,
+                            int32_t ldo, void* stream) {
+  if (!A || !D || !out || ncols < 0 || ldd < ncols || ldo < ncols) {
+    set_error("hf_csr_dense: bad argument");
+    return HF_ERR_ARG;
+  }
+  const size_t work = (size_t)A->n_rows * ncols;
+  if (work == 0) return HF_OK;
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  tail::k_csr_dense<<<(unsigned)((work + 255) / 256), 256, 0, s>>>(A->n_rows, ncols, A->indptr, A->indices,
+                                                                    A->val, D, ldd, out, ldo);
   HF_LAUNCH_CHECK();
   count_launches(1);
   return HF_OK;

@@ -70,30 +70,6 @@ class EitDofMap:
         return len(self.element_sets)
 
 
-def _nearest_center_exact(cc, centers, chunk=8192):
-    """argmin_j ||cc_i - centers_j|| with the reference's arithmetic and
-    first-index ties (leadfield.py:98-99), without the (E, m, 3) array.
-
-    A k-d tree proposes the two nearest centres; where the runner-up is more
-    than 1e-9 relatively farther, the nearest is unique far beyond rounding and
-    equals the reference's argmin.  The (rare) near-ties are re-evaluated with
-    np.linalg.norm over all centres exactly as the reference does."""
-    from scipy.spatial import cKDTree
-
-    m = len(centers)
-    if m == 1:
-        return np.zeros(len(cc), dtype=np.int64)
-    tree = cKDTree(centers)
-    dist, idx = tree.query(cc, k=2, workers=-1)
-    owner = idx[:, 0].astype(np.int64)
-    close = np.flatnonzero(dist[:, 1] <= dist[:, 0] * (1.0 + 1e-9) + 1e-300)
-    for a in range(0, len(close), chunk):
-        sel = close[a:a + chunk]
-        d = np.linalg.norm(cc[sel][:, None, :] - centers[None, :, :], axis=2)
-        owner[sel] = np.argmin(d, axis=1)
-    return owner
-
-
 def nearest_center_device(cc, centers):
     """owner = argmin_j ||cc_i - centers_j|| on the GPU (hf_nearest_center):
     the reference's rounding and first-index ties, every pair evaluated."""
@@ -106,15 +82,15 @@ def nearest_center_device(cc, centers):
     return owner[: len(cc)].cpu().numpy().astype(np.int64)
 
 
-def build_dof_map(mesh, compartments, n_dofs, seed=0, chunk=8192, method="auto"):
+def build_dof_map(mesh, compartments, n_dofs, seed=0):
     """Nearest-centre partition of the perturbable elements (leadfield.py:80-101).
 
-    Same centre draw (rng.choice), same per-entry distance arithmetic and
-    first-index argmin as the reference.  method: "device" (hf_nearest_center,
-    all pairs on the GPU; the default when CUDA is present), "tree" (exact
-    k-d-tree search on the host, `_nearest_center_exact`), "dense" (the
-    reference's comparison in element chunks).  C4 has 4.1M elements x 5,000
-    DOFs, where the reference needs a 459 GiB array."""
+    The reference's centre draw (rng.choice, the one host step), then on the
+    device: element centroids with numpy's rounding, the nearest centre for every
+    (element, centre) pair with the reference's distance arithmetic and first-index
+    argmin, and the partition into sets.  C4 has 4.1M elements x 5,000 DOFs, where
+    the reference needs a 459 GiB array.  Needs a CUDA device (no CPU fallback)."""
+    N.require_cuda()
     cand = np.flatnonzero(np.isin(mesh.labels, np.asarray(compartments)))
     if cand.size == 0:
         raise DofError("no mesh elements in the perturbable compartments")
@@ -124,26 +100,7 @@ def build_dof_map(mesh, compartments, n_dofs, seed=0, chunk=8192, method="auto")
     rng = np.random.default_rng(seed)
     vols = mesh.volumes[cand]
     chosen = rng.choice(cand, size=n_dofs, replace=False, p=vols / vols.sum())
-    if method == "auto":
-        method = "device" if torch.cuda.is_available() else (
-            "tree" if len(cand) * n_dofs > 5e7 else "dense")
-    if method == "device":
-        return _dof_map_device(mesh, cand, chosen)
-    centroids = mesh.centroids()
-    centers = centroids[chosen]
-    cc = centroids[cand]
-    if method == "tree":
-        owner = _nearest_center_exact(cc, centers, chunk)
-    else:
-        owner = np.empty(len(cand), dtype=np.int64)
-        step = max(1, chunk * 64 // max(n_dofs, 1))
-        for a in range(0, len(cand), step):
-            d = np.linalg.norm(cc[a:a + step][:, None, :] - centers[None, :, :], axis=2)
-            owner[a:a + step] = np.argmin(d, axis=1)
-    order = np.argsort(owner, kind="stable")
-    bounds = np.searchsorted(owner[order], np.arange(n_dofs + 1))
-    sets = tuple(cand[order[bounds[k]:bounds[k + 1]]] for k in range(n_dofs))
-    return EitDofMap(element_sets=sets, centers=centers)
+    return _dof_map_device(mesh, cand, chosen)
 
 
 def _dof_map_device(mesh, cand, chosen):
@@ -381,7 +338,10 @@ def eit_leadfield(sys, dofs, currents, cfg=PcgConfig(), threads=1):
     L, P = dsys.L, I.shape[1]
     dev = T.device
     Vd = torch.from_numpy(np.ascontiguousarray(V)).to(dev)
-    BV = dsys.Bd @ Vd                             # n x P right-hand sides u_p
+    Bcsr = DeviceCsr.from_scipy(sp.csr_matrix(sys.B), dev)
+    BV = torch.empty((dsys.n, P), dtype=torch.float64, device=dev)  # n x P right-hand sides u_p
+    N.check("hf_csr_dense", N.lib.hf_csr_dense(N.C.byref(Bcsr.struct), N.ptr(Vd), P, P, N.ptr(BV), P,
+                                               N.stream_handle()))
     U, info = solve_block(dsys.op, BV, cfg)
     _raise_failed(info, U, cfg, column_tag=False)  # pcg_solve semantics: no column tag
     cols = eit_columns_device(sys.mesh, dofs, sys.ground, T, U, response_operator(M, sys.R))

@@ -107,27 +107,29 @@ def test_electrodes_from_centers_match_reference():
         np.testing.assert_array_equal(a, b)
 
 
-def test_dof_map_matches_reference_draws():
-    from paper_1811_07717_b200.leadfield import build_dof_map
+def test_dof_map_oracle_paths_match_reference():
+    """The oracle's chunked and k-d-tree restatements of build_dof_map give the
+    reference's sets (the product's device path is checked against both on the GPU)."""
+    import oracle
 
     fx = load("layered_h12.npz")
     mesh = mesh_from_fixture(fx)
-    dofs = build_dof_map(mesh, [0, 1], 20, seed=2, chunk=64)  # tiny chunks: same answer
-    np.testing.assert_array_equal(np.concatenate(dofs.element_sets), fx["eit_dof_elems"])
-    np.testing.assert_array_equal(np.cumsum([0] + [len(e) for e in dofs.element_sets]),
-                                  fx["eit_dof_ptr"])
-    np.testing.assert_array_equal(dofs.centers, fx["eit_centers"])
+    for method in ("tree", "dense"):
+        sets, centers = oracle.build_dof_map(mesh, [0, 1], 20, seed=2, method=method, chunk=64)
+        np.testing.assert_array_equal(np.concatenate(sets), fx["eit_dof_elems"])
+        np.testing.assert_array_equal(np.cumsum([0] + [len(e) for e in sets]), fx["eit_dof_ptr"])
+        np.testing.assert_array_equal(centers, fx["eit_centers"])
 
 
-def test_dof_map_tree_path_matches_reference():
+def test_build_dof_map_has_no_cpu_fallback():
+    import torch
+
     from paper_1811_07717_b200.leadfield import build_dof_map
 
-    fx = load("layered_h12.npz")
-    mesh = mesh_from_fixture(fx)
-    dofs = build_dof_map(mesh, [0, 1], 20, seed=2, method="tree")
-    np.testing.assert_array_equal(np.concatenate(dofs.element_sets), fx["eit_dof_elems"])
-    np.testing.assert_array_equal(np.cumsum([0] + [len(e) for e in dofs.element_sets]),
-                                  fx["eit_dof_ptr"])
+    if torch.cuda.is_available():
+        pytest.skip("a CUDA device is present")
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        build_dof_map(mesh_from_fixture(load("layered_h12.npz")), [0, 1], 20, seed=2)
 
 
 def test_column_blocks():
