@@ -652,7 +652,10 @@ def run_reference(args):
     log(f"[reference] {hf.__file__}: mesh {mesh.n_nodes} nodes, assemble_A nnz {A.nnz} in {t_setup:.1f}s")
     _REF["A"], _REF["B"] = A, B
     L = B.shape[1]
-    cores = int(args.ref_cores or os.cpu_count() or 1)
+    # every host core (16 on this pool's boxes), capped at 32 processes: each step is one
+    # whole column per process, and past ~32 processes the shared memory bandwidth makes
+    # a step (and the 20-step run) longer without more columns per second
+    cores = int(args.ref_cores or min(os.cpu_count() or 1, 32))
     cores = max(1, min(cores, L))
     ctx = mp.get_context("fork")
     walls, its = [], []
