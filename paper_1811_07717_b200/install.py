@@ -14,20 +14,33 @@ _PATCHES = {
     "solver": ("ldp", "pcg_solve", "transfer_matrix"),
     "fem": ("stiffness_blocks", "volume_stiffness", "assemble_A"),
     "leadfield": ("stiffness_blocks", "pcg_solve", "transfer_matrix", "electrode_response",
-                  "eeg_leadfield", "eit_forward", "eit_leadfield"),
+                  "eeg_leadfield", "eit_forward", "eit_leadfield", "build_dof_map"),
     "cli": ("eeg_leadfield", "eit_leadfield", "eit_forward", "assemble_A", "transfer_matrix",
-            "generate_mesh"),
-    "experiments": ("eeg_leadfield", "eit_leadfield", "eit_forward", "assemble_A", "generate_mesh"),
+            "generate_mesh", "build_dof_map"),
+    "experiments": ("eeg_leadfield", "eit_leadfield", "eit_forward", "assemble_A", "generate_mesh",
+                    "build_dof_map"),
     "meshgen": ("generate_mesh",),
     "simulate": ("eit_forward", "assemble_A", "eeg_leadfield"),
     "": ("ldp", "pcg_solve", "transfer_matrix", "assemble_A", "volume_stiffness",
-         "eeg_leadfield", "eit_forward", "eit_leadfield", "electrode_response", "generate_mesh"),
+         "eeg_leadfield", "eit_forward", "eit_leadfield", "electrode_response", "generate_mesh",
+         "build_dof_map"),
 }
 _saved = []
 
 
 def _engine(name, headfem=None):
     from . import fem, leadfield, meshgen, solver
+    if name == "build_dof_map":  # returns the caller's own EitDofMap type
+        dof_cls = importlib.import_module(f"{headfem.__name__}.leadfield").EitDofMap
+
+        def build_dof_map(mesh, compartments, n_dofs, seed=0):
+            m = leadfield.build_dof_map(mesh, compartments, n_dofs, seed)
+            out = dof_cls(element_sets=m.element_sets, centers=m.centers)
+            object.__setattr__(out, "_device", getattr(m, "_device", None))  # the device arrays
+            return out
+
+        build_dof_map.__doc__ = leadfield.build_dof_map.__doc__
+        return build_dof_map
     if name == "generate_mesh":  # returns the caller's own TetMesh type
         mesh_cls = importlib.import_module(f"{headfem.__name__}.meshgen").TetMesh
 
