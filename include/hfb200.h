@@ -17,6 +17,7 @@
  *   hf_csr_bandwidth       (internal)          gather reach of A, sizes the PCG batch width
  *   hf_pcg_multi           solver.py:64-111    pcg_solve(A, b, cfg), one column per RHS
  *                          solver.py:114-141   transfer_matrix(A, B, cfg, threads)
+ *   hf_pcg_stream          solver.py:114-141   transfer_matrix with columns streamed through kp slots
  *   hf_pcg_profile         (bench)             per-kernel CUDA-event timing of a PCG round
  *   hf_csr_prune_*         (internal)          zero-free copy of A for the SpMM
  *   hf_p1_blocks           fem.py:31-93        element_gradients + stiffness_blocks
@@ -139,6 +140,21 @@ int hf_pcg_multi(const hf_csr* A, const double* d, const double* B, int32_t n, i
                  double tol, int32_t max_iter, const int32_t* freeze_at, double* X,
                  int32_t* iters, int32_t* status, double* true_res, double* best_res,
                  int32_t* best_iter, void* ws, size_t ws_bytes, void* stream);
+
+/* Column streaming: the same solver for ncols >= 1 columns of B (device n x ldb
+ * row-major, columns 0..ncols-1) through kp slots.  When a slot's column finishes,
+ * its x goes to column j of X (device n x ldb) and the slot takes the next column
+ * at the next chunk boundary, so no slot waits for the slowest column of a batch.
+ * Per-column iterates are bit-identical to hf_pcg_multi's (canonical reductions).
+ * iters, status, best_iter (int32) and true_res, best_res (double): host, ncols
+ * each.  FAILED columns hold x at max_iter: replay them with hf_pcg_multi and
+ * freeze_at = best_iter for the best iterate (solver.py:92-93, 108-111).
+ * Workspace: hf_pcg_stream_workspace_bytes(n, kp, ncols). */
+size_t hf_pcg_stream_workspace_bytes(int32_t n, int32_t kp, int32_t ncols);
+int hf_pcg_stream(const hf_csr* A, const double* d, const double* B, int32_t ldb, int32_t ncols,
+                  int32_t n, int32_t kp, double tol, int32_t max_iter, double* X, int32_t* iters,
+                  int32_t* status, double* true_res, double* best_res, int32_t* best_iter,
+                  void* ws, size_t ws_bytes, void* stream);
 
 /* Timing probe for the roofline report: runs `rounds` PCG rounds of the same
  * kernels as hf_pcg_multi (tolerance 0, so no column stops) and writes the

@@ -51,6 +51,8 @@ def _load():
         "hf_pcg_workspace_bytes": (SZ, [I32, I32, I64]),
         "hf_pcg_multi": (C.c_int, [pcsr, P, P, I32, I32, D, I32, P, P, P, P, P, P, P, P, SZ, P]),
         "hf_pcg_profile": (C.c_int, [pcsr, P, P, I32, I32, I32, P, P, C.POINTER(I32), P, SZ, P]),
+        "hf_pcg_stream_workspace_bytes": (SZ, [I32, I32, I32]),
+        "hf_pcg_stream": (C.c_int, [pcsr, P, P, I32, I32, I32, I32, D, I32, P, P, P, P, P, P, P, SZ, P]),
         "hf_p1_blocks": (C.c_int, [P, P, I32, P, I32, P, I32, D, P, P, C.POINTER(I32), P]),
         "hf_p1_assemble_workspace_bytes": (SZ, [I32, I32, I32]),
         "hf_p1_assemble_prepare": (C.c_int, [P, I32, I32, P, I32, I32, P, C.POINTER(I64), P, SZ, P]),
@@ -94,7 +96,8 @@ lib = _load()
 EXPORTED = ("hf_version", "hf_last_error", "hf_device_sm_count", "hf_launch_count", "hf_scan_workspace_bytes",
             "hf_exclusive_scan_i32", "hf_ldp", "hf_csr_bandwidth",
             "hf_csr_prune_workspace_bytes", "hf_csr_prune_count", "hf_csr_prune_fill",
-            "hf_pcg_workspace_bytes", "hf_pcg_multi", "hf_pcg_profile", "hf_p1_blocks",
+            "hf_pcg_workspace_bytes", "hf_pcg_multi", "hf_pcg_profile", "hf_pcg_stream_workspace_bytes",
+            "hf_pcg_stream", "hf_p1_blocks",
             "hf_p1_assemble_workspace_bytes", "hf_p1_assemble_prepare", "hf_p1_assemble_fill",
             "hf_response_matrix", "hf_lf_tail", "hf_dense_lf", "hf_csr_dense", "hf_eit_sens_workspace_bytes", "hf_eit_sens",
             "hf_topology_workspace_bytes", "hf_boundary_faces", "hf_whitney_gt",

@@ -365,6 +365,103 @@ __global__ void __launch_bounds__(Map<KP>::NT)
   if (tid == 0) c.summary[SUM_REPLACE] = 0;
 }
 
+// ---------------------------------------------------------------- column streaming
+// hf_pcg_stream runs more columns than the kp slots of a batch: a slot whose
+// column finished is harvested (its x and results copied out) and refilled with
+// the next column at a chunk boundary, so no slot idles while the slowest column
+// of a batch finishes.  k_refill is k_init restricted to the refilled slots
+// (slot[j] = source column, -2 = no column left: b = 0, state ZERO; -1 = keep):
+// the same per-row arithmetic and the same canonical b.b / b.z reductions, so a
+// column's iterates are bit-identical to a batch solve of it.
+template <int KP>
+__global__ void __launch_bounds__(Map<KP>::NT)
+    k_refill(Ctl c, const int* __restrict__ slot_col, const double* __restrict__ Ball, int ldb,
+             double* Bs, const double* __restrict__ d, double* X, double* R, double* P, int init_dd) {
+  using M = Map<KP>;
+  __shared__ double sm[M::RED];
+  __shared__ double tot[2 * KP];
+  __shared__ int s_col[KP];
+  const int tid = threadIdx.x, grp = tid / M::LPR, glane = tid % M::LPR;
+  for (int j = tid; j < KP; j += M::NT) s_col[j] = slot_col[j];
+  __syncthreads();
+  int col[M::CPL];
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) {
+    col[k] = s_col[glane * M::CPL + k];
+    any |= col[k] != -1;
+  }
+  const int nt = n_tiles(c.n);
+  double v[2][M::CPL];
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) v[0][k] = v[1][k] = 0.0;
+  if (any || init_dd) {
+    for (int t = blockIdx.x; t < nt; t += c.G) {
+      const int row = t * TR + grp;
+      if (row >= c.n) continue;
+      const size_t o = (size_t)row * KP + glane * M::CPL;
+      const double dd = d[row];
+      if (init_dd && glane == 0) c.dd[row] = make_double2(dd, 1.0 / dd);
+#pragma unroll
+      for (int k = 0; k < M::CPL; ++k) {
+        if (col[k] == -1) continue;
+        const double b = col[k] >= 0 ? Ball[(size_t)row * ldb + col[k]] : 0.0;
+        const double z = __ddiv_rn(b, dd);
+        v[0][k] = dot_acc(v[0][k], b, b);
+        v[1][k] = dot_acc(v[1][k], b, z);
+        Bs[o + k] = b;
+        X[o + k] = 0.0;
+        R[o + k] = b;
+        P[o + k] = z;
+      }
+    }
+  }
+  block_partials<M, 2>(v, sm, c);
+  if (!last_block_reduce<M, 2>(c, sm, tot)) return;
+  int st = -1;
+  if (tid < KP) {
+    const int j = tid;
+    st = c.state[j];
+    if (s_col[j] != -1) {
+      const double nb = sqrt(tot[j]);
+      c.normb[j] = nb;
+      c.rz[j] = tot[KP + j];
+      c.beta[j] = 0.0;
+      c.best_res[j] = 1.0;
+      c.best_iter[j] = 0;
+      c.iters[j] = 0;
+      c.true_res[j] = 0.0;
+      c.pmask[j] = 0;
+      st = nb == 0.0 ? S_ZERO : S_RUN;
+      c.state[j] = st;
+    }
+  }
+  census<KP>(c, st);
+}
+
+// Copy the finished slots' x into their columns of Xall and their results into
+// per-column arrays (slot_col[j] = destination column, -1 = none).
+template <int KP>
+__global__ void k_harvest(Ctl c, const int* __restrict__ slot_col, const double* __restrict__ X,
+                          double* Xall, int ldx, int* r_iters, int* r_state, double* r_true,
+                          double* r_best, int* r_best_it) {
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < KP) {
+    const int col = slot_col[t];
+    if (col >= 0) {
+      r_iters[col] = c.iters[t];
+      r_state[col] = c.state[t];
+      r_true[col] = c.true_res[t];
+      r_best[col] = c.best_res[t];
+      r_best_it[col] = c.best_iter[t];
+    }
+  }
+  if (t >= (size_t)c.n * KP) return;
+  const int row = (int)(t / KP), j = (int)(t % KP);
+  const int col = slot_col[j];
+  if (col >= 0) Xall[(size_t)row * ldx + col] = X[t];
+}
+
 // ---------------------------------------------------------------- SpMM over an ELL copy
 // The SpMM runs on a padded ELL copy of the zero-free matrix (8 slots per row,
 // built once per solve by k_ell_fill).  Empty slots 0..ELL_OPT-1 hold (row
@@ -1276,6 +1373,153 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
   return HF_OK;
 }
 
+// Column streaming (hf_pcg_stream): L >= 1 columns of Ball through kp slots.  The
+// host keeps LOOKAHEAD chunks queued; when a status read shows finished slots it
+// enqueues, behind the queued chunks, one harvest (x and results out) and one
+// refill (the next columns in, or b = 0 when none is left).  Terminal states never
+// change, so the queued chunks leave those slots alone until then.
+template <int KP>
+int run_stream(const hf_csr* A, const double* d, const double* Ball, int ldb, int ncols, int n,
+               double tol, int max_iter, double* Xall, int32_t* iters, int32_t* status,
+               double* true_res, double* best_res, int32_t* best_iter, void* ws, size_t ws_bytes,
+               cudaStream_t stream) {
+  using M = Map<KP>;
+  Layout L = carve(ws, n, KP);
+  Carve cv{reinterpret_cast<char*>(ws), L.bytes, ~size_t(0)};
+  double* Bs = cv.take<double>((size_t)n * KP);  // the slots' right-hand sides (check path)
+  double* X = cv.take<double>((size_t)n * KP);
+  int* d_refill = cv.take<int>(KP);
+  int* d_harvest = cv.take<int>(KP);
+  int* r_it = cv.take<int>(ncols);
+  int* r_st = cv.take<int>(ncols);
+  int* r_bi = cv.take<int>(ncols);
+  double* r_tr = cv.take<double>(ncols);
+  double* r_br = cv.take<double>(ncols);
+  if (cv.used + 256 > ws_bytes) {
+    set_error("pcg stream workspace too small: need %zu, have %zu", cv.used + 256, ws_bytes);
+    return HF_ERR_WORKSPACE;
+  }
+  Grids g;
+  if (int rc = setup<KP>(L, A, n, tol, max_iter, g, stream)) return rc;
+  cudaStream_t cap = nullptr;
+  int* h_sum = nullptr;
+  if (int rc = thread_resources(&cap, &h_sum)) return rc;
+  int* h_state = nullptr;  // per-slot states of the status read (pinned, freed on return)
+  HF_CUDA(cudaHostAlloc(&h_state, sizeof(int) * KP, cudaHostAllocPortable));
+  struct Guard {
+    int* hs;
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    cudaEvent_t ev[LOOKAHEAD + 1] = {};
+    ~Guard() {
+      if (ge) cudaGraphExecDestroy(ge);
+      if (g) cudaGraphDestroy(g);
+      for (auto e : ev)
+        if (e) cudaEventDestroy(e);
+      if (hs) cudaFreeHost(hs);
+    }
+  } guard{h_state};
+  HF_CUDA(cudaMemsetAsync(L.counter, 0, sizeof(unsigned int) * 4, stream));
+  HF_CUDA(cudaMemsetAsync(L.xmask, 0, sizeof(int) * (XD + 1) * KP, stream));
+  HF_CUDA(cudaMemsetAsync(L.summary, 0, sizeof(int) * SUM_N, stream));
+  HF_CUDA(cudaMemsetAsync(L.state, 0, sizeof(int) * KP, stream));
+  std::vector<int> slot_col(KP, -1), refill(KP), harvest(KP);
+  int next = 0;
+  for (int j = 0; j < KP; ++j) {
+    refill[j] = next < ncols ? next : -2;
+    slot_col[j] = refill[j] >= 0 ? refill[j] : -1;
+    if (next < ncols) ++next;
+  }
+  auto enqueue_refill = [&](int init_dd) -> int {
+    HF_CUDA(cudaMemcpyAsync(d_refill, refill.data(), sizeof(int) * KP, cudaMemcpyHostToDevice, stream));
+    k_refill<KP><<<g.c.G, M::NT, 0, stream>>>(g.c, d_refill, Ball, ldb, Bs, d, X, L.R, L.P, init_dd);
+    HF_LAUNCH_CHECK();
+    count_launches(1);
+    // the staging array must not change before the copy ran
+    HF_CUDA(cudaStreamSynchronize(stream));
+    return HF_OK;
+  };
+  if (int rc = enqueue_refill(1)) return rc;
+  HF_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+  for (int r = 0; r < CHUNK; ++r) launch_round<KP>(g, L, X, r, cap, nullptr);
+  launch_check<KP>(g, L, Bs, X, cap);
+  cudaMemcpyAsync(h_sum, L.summary, sizeof(int) * SUM_N, cudaMemcpyDeviceToHost, cap);
+  cudaMemcpyAsync(h_state, L.state, sizeof(int) * KP, cudaMemcpyDeviceToHost, cap);
+  const cudaError_t le = cudaGetLastError();
+  const cudaError_t ce = cudaStreamEndCapture(cap, &guard.g);
+  if (ce != cudaSuccess || le != cudaSuccess) {
+    set_error("graph capture failed: %s / %s", cudaGetErrorString(ce), cudaGetErrorString(le));
+    return HF_ERR_CUDA;
+  }
+  HF_CUDA(cudaGraphInstantiate(&guard.ge, guard.g, 0));
+  for (auto& e : guard.ev) HF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  // every column needs at most max_iter + 1 chunks in its slot and waits at most
+  // LOOKAHEAD + 1 chunks for a refill
+  const long per_col = (long)max_iter + 2 * LOOKAHEAD + 8;
+  const long max_chunks = per_col * ((ncols + KP - 1) / KP + 1);
+  // A status read after chunk r may be newer but is never older; a slot refilled
+  // behind chunk f is only trusted from the read of chunk f + 1 on.
+  std::vector<long> fresh_from(KP, 0);
+  int harvested = 0;
+  long i = 0;
+  for (; i < max_chunks && harvested < ncols; ++i) {
+    HF_CUDA(cudaGraphLaunch(guard.ge, stream));
+    count_launches(PER_CHUNK);
+    HF_CUDA(cudaEventRecord(guard.ev[i % (LOOKAHEAD + 1)], stream));
+    if (i < LOOKAHEAD) continue;
+    const long r = i - LOOKAHEAD;
+    HF_CUDA(cudaEventSynchronize(guard.ev[r % (LOOKAHEAD + 1)]));
+    bool any = false;
+    for (int j = 0; j < KP; ++j) {
+      const int st = ((volatile int*)h_state)[j];
+      const bool done = st == S_DONE || st == S_FAILED || st == S_ZERO;
+      harvest[j] = (r >= fresh_from[j] && done && slot_col[j] >= 0) ? slot_col[j] : -1;
+      refill[j] = -1;
+      if (harvest[j] >= 0) {
+        any = true;
+        ++harvested;
+        refill[j] = next < ncols ? next : -2;
+        slot_col[j] = next < ncols ? next : -1;
+        if (next < ncols) ++next;
+        fresh_from[j] = i + 1;
+      }
+    }
+    if (!any) continue;
+    // behind the queued chunks: harvest, then refill
+    HF_CUDA(cudaMemcpyAsync(d_harvest, harvest.data(), sizeof(int) * KP, cudaMemcpyHostToDevice, stream));
+    const size_t work = (size_t)n * KP;
+    k_harvest<KP><<<(unsigned)((work + 255) / 256), 256, 0, stream>>>(g.c, d_harvest, X, Xall, ldb, r_it,
+                                                                      r_st, r_tr, r_br, r_bi);
+    HF_LAUNCH_CHECK();
+    count_launches(1);
+    if (int rc = enqueue_refill(0)) return rc;
+  }
+  HF_CUDA(cudaStreamSynchronize(stream));
+  if (harvested < ncols) {
+    set_error("pcg stream control did not finish: %d of %d columns after %ld chunks", harvested, ncols, i);
+    return HF_ERR_INTERNAL;
+  }
+  HF_CUDA(cudaMemcpyAsync(iters, r_it, sizeof(int) * ncols, cudaMemcpyDeviceToHost, stream));
+  HF_CUDA(cudaMemcpyAsync(status, r_st, sizeof(int) * ncols, cudaMemcpyDeviceToHost, stream));
+  HF_CUDA(cudaMemcpyAsync(true_res, r_tr, sizeof(double) * ncols, cudaMemcpyDeviceToHost, stream));
+  HF_CUDA(cudaMemcpyAsync(best_res, r_br, sizeof(double) * ncols, cudaMemcpyDeviceToHost, stream));
+  HF_CUDA(cudaMemcpyAsync(best_iter, r_bi, sizeof(int) * ncols, cudaMemcpyDeviceToHost, stream));
+  HF_CUDA(cudaStreamSynchronize(stream));
+  return HF_OK;
+}
+
+inline size_t stream_bytes(int n, int kp, int ncols) {
+  Layout L = carve(nullptr, n, kp);
+  Carve cv{nullptr, L.bytes, ~size_t(0)};
+  cv.take<double>((size_t)n * kp);
+  cv.take<double>((size_t)n * kp);
+  cv.take<int>(kp);
+  cv.take<int>(kp);
+  for (int q = 0; q < 3; ++q) cv.take<int>(ncols);
+  for (int q = 0; q < 2; ++q) cv.take<double>(ncols);
+  return cv.used + 512;
+}
+
 // Per-kernel timing of `rounds` PCG rounds with CUDA events on the launch
 // stream (bench.py roofline).  tol = 0 keeps every column running.  ms3 =
 // {k_spmm, k_update_r, k_update_p / k_update_xring averaged over the ring}.
@@ -1401,6 +1645,42 @@ extern "C" int hf_pcg_multi(const hf_csr* A, const double* d, const double* B, i
       return HF_ERR_ARG;
   }
 #undef HF_PCG_CASE
+}
+
+extern "C" size_t hf_pcg_stream_workspace_bytes(int32_t n, int32_t kp, int32_t ncols) {
+  return pcg::stream_bytes(n, kp, ncols);
+}
+
+extern "C" int hf_pcg_stream(const hf_csr* A, const double* d, const double* B, int32_t ldb,
+                             int32_t ncols, int32_t n, int32_t kp, double tol, int32_t max_iter,
+                             double* X, int32_t* iters, int32_t* status, double* true_res,
+                             double* best_res, int32_t* best_iter, void* ws, size_t ws_bytes,
+                             void* stream) {
+  if (!A || !d || !B || !X || !iters || !status || !true_res || !best_res || !best_iter || !ws) {
+    set_error("hf_pcg_stream: null argument");
+    return HF_ERR_ARG;
+  }
+  if (n <= 0 || A->n_rows != n || A->n_cols != n || max_iter < 1 || !(tol > 0.0) || ncols < 1 ||
+      ldb < ncols) {
+    set_error("hf_pcg_stream: bad shape or settings (n=%d ncols=%d ldb=%d)", n, ncols, ldb);
+    return HF_ERR_ARG;
+  }
+  if (n >= (1 << 30)) {
+    set_error("hf_pcg_stream: n=%d exceeds the ELL column range", n);
+    return HF_ERR_ARG;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+#define HF_STREAM_CASE(K)                                                                      \
+  case K:                                                                                      \
+    return pcg::run_stream<K>(A, d, B, ldb, ncols, n, tol, max_iter, X, iters, status,         \
+                              true_res, best_res, best_iter, ws, ws_bytes, s);
+  switch (kp) {
+    HF_PCG_WIDTHS(HF_STREAM_CASE)
+    default:
+      set_error("hf_pcg_stream: unsupported kp=%d", kp);
+      return HF_ERR_ARG;
+  }
+#undef HF_STREAM_CASE
 }
 
 extern "C" int hf_pcg_profile(const hf_csr* A, const double* d, const double* B, int32_t n,

@@ -117,6 +117,8 @@ def solve_block(op, B, cfg=PcgConfig(), batch=MAX_BATCH, out=None):
     info = SolveInfo(np.zeros(k, np.int64), np.zeros(k, np.int64), np.zeros(k), np.ones(k),
                      np.zeros(k, np.int64), max_iter)
     batch = max(1, op.batch_width(k, batch))
+    if k > batch:  # more columns than slots: stream them through the slots
+        return _solve_streamed(op, B, cfg, width_for(batch), max_iter, X, info)
     for c0 in range(0, k, batch):
         c1 = min(k, c0 + batch)
         kb = c1 - c0
@@ -137,6 +139,46 @@ def solve_block(op, B, cfg=PcgConfig(), batch=MAX_BATCH, out=None):
         info.true_residual[c0:c1] = tr[:kb]
         info.best_residual[c0:c1] = br[:kb]
         info.best_iteration[c0:c1] = bi[:kb]
+    return X, info
+
+
+def _solve_streamed(op, B, cfg, kp, max_iter, X, info):
+    """hf_pcg_stream: the k columns of B flow through kp slots, a finished column's
+    slot taking the next one at a chunk boundary (no slot waits for the slowest
+    column of a batch).  A column's iterates are bit-identical to a batch solve;
+    failed columns are replayed to their best iterate in batches."""
+    n, k = B.shape
+    Bc = B if B.is_contiguous() else B.contiguous()
+    if not X.is_contiguous():
+        raise ValueError("output block must be contiguous")
+    ws = torch.empty(N.lib.hf_pcg_stream_workspace_bytes(n, kp, k), dtype=torch.uint8, device=B.device)
+    it = np.zeros(k, dtype=np.int32)
+    stt = np.zeros(k, dtype=np.int32)
+    tr = np.zeros(k, dtype=np.float64)
+    br = np.zeros(k, dtype=np.float64)
+    bi = np.zeros(k, dtype=np.int32)
+    P = N.C.c_void_p
+    N.check("hf_pcg_stream", N.lib.hf_pcg_stream(
+        N.C.byref(op.Ac.struct), N.ptr(op.d), N.ptr(Bc), k, k, n, kp, float(cfg.tolerance), int(max_iter),
+        N.ptr(X), P(it.ctypes.data), P(stt.ctypes.data), P(tr.ctypes.data), P(br.ctypes.data),
+        P(bi.ctypes.data), N.ptr(ws), ws.numel(), N.stream_handle()))
+    del ws
+    failed = np.flatnonzero(stt == N.HF_COL_FAILED)
+    for f0 in range(0, failed.size, kp):
+        cols = failed[f0:f0 + kp]
+        kw = width_for(max(len(cols), 2))
+        Bb = torch.zeros((n, kw), dtype=torch.float64, device=B.device)
+        idx = torch.from_numpy(cols).to(B.device)
+        Bb[:, :len(cols)] = Bc[:, idx]
+        freeze = np.zeros(kw, dtype=np.int32)  # other slots stop at x = 0
+        freeze[:len(cols)] = bi[cols]
+        Xr = _run_batch(op, Bb, cfg.tolerance, max_iter, freeze=freeze)[0]
+        X[:, idx] = Xr[:, :len(cols)]
+    info.iterations[:] = it
+    info.status[:] = stt
+    info.true_residual[:] = tr
+    info.best_residual[:] = br
+    info.best_iteration[:] = bi
     return X, info
 
 

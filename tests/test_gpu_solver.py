@@ -302,6 +302,77 @@ class TestTransferMatrix:
                 assert info.true_residual[l] <= tol
 
 
+class TestStream:
+    """hf_pcg_stream (columns streamed through kp slots) against batch solves:
+    every column's x and per-column results bit-identical."""
+
+    @staticmethod
+    def _solve(A, B, cfg, batch):
+        from paper_1811_07717_b200.solver import operator, rhs_block, solve_block
+
+        X, info = solve_block(operator(A, cfg), rhs_block(B), cfg, batch=batch)
+        return X.cpu().numpy(), info
+
+    @staticmethod
+    def _same(a, b):
+        Xa, ia = a
+        Xb, ib = b
+        np.testing.assert_array_equal(Xa, Xb)
+        for f in ("iterations", "status", "true_residual", "best_residual", "best_iteration"):
+            np.testing.assert_array_equal(getattr(ia, f), getattr(ib, f), err_msg=f)
+
+    @pytest.mark.parametrize("slots", [2, 8, 32])
+    def test_stream_equals_batch(self, eng, slots):
+        from tests.fixtures import csr
+
+        fx = load("layered_h14_tensor.npz")
+        A = csr(fx, "A")
+        rng = np.random.default_rng(slots)
+        k = 45
+        B = rng.normal(size=(A.shape[0], k)) * np.geomspace(1e-3, 1e3, k)
+        B[:, ::7] *= rng.uniform(0, 1, size=(A.shape[0], 1)) ** 8   # harder columns
+        B[fx["ground"]] = 0.0
+        B[:, [0, 11, 44]] = 0.0                                      # zero columns, first and last
+        cfg = eng.PcgConfig(tolerance=1e-10)
+        ref = self._solve(A, B, cfg, 64)
+        got = self._solve(A, B, cfg, slots)
+        self._same(got, ref)
+        assert (ref[1].status == eng._native.HF_COL_ZERO).sum() == 3
+
+    def test_stream_failed_columns_replay_best_iterate(self, eng):
+        from tests.fixtures import csr
+
+        fx = load("layered_h14_tensor.npz")
+        A = csr(fx, "A")
+        rng = np.random.default_rng(5)
+        B = rng.normal(size=(A.shape[0], 30))
+        B[fx["ground"]] = 0.0
+        full = self._solve(A, B, eng.PcgConfig(tolerance=1e-12), 64)[1].iterations
+        cap = int(np.median(full))
+        cfg = eng.PcgConfig(tolerance=1e-12, max_iterations=cap)
+        ref = self._solve(A, B, cfg, 64)
+        fails = (ref[1].status == eng._native.HF_COL_FAILED).sum()
+        assert 0 < fails < 30
+        self._same(self._solve(A, B, cfg, 4), ref)
+
+    def test_stream_fewer_columns_than_slots(self, eng):
+        from paper_1811_07717_b200.solver import _solve_streamed, operator, rhs_block, SolveInfo
+        from tests.fixtures import csr
+
+        fx = load("layered_h12.npz")
+        A, B = csr(fx, "A"), csr(fx, "B").toarray()[:, :3]
+        cfg = eng.PcgConfig(tolerance=1e-10)
+        op = operator(A, cfg)
+        Bd = rhs_block(B)
+        n, k = Bd.shape
+        mi = int(cfg.resolve_max_iterations(n))
+        X = Bd.new_empty((n, k))
+        info = SolveInfo(np.zeros(k, np.int64), np.zeros(k, np.int64), np.zeros(k), np.ones(k),
+                         np.zeros(k, np.int64), mi)
+        X, info = _solve_streamed(op, Bd, cfg, 16, mi, X, info)
+        self._same((X.cpu().numpy(), info), self._solve(A, B, cfg, 64))
+
+
 def test_csr_bandwidth_and_batch_width(cuda):
     """hf_csr_bandwidth = max_i max(i - first col, last col - i) of the SpMM copy;
     the batch width follows it (PcgOperator.batch_width)."""
