@@ -119,6 +119,18 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- our arm
+def _nnz(A):
+    return int(A.nnz) if hasattr(A, "nnz") else int(A.indices.numel())
+
+
+def survey_round(n, nnz_stored, kp, round_ms, peak):
+    """bytes_per_rhs_iter(k) = 80 n + (12 nnz + 4 (n+1) + 16 n) / k."""
+    per = 80 * n + (12 * nnz_stored + 4 * (n + 1) + 16 * n) / kp
+    gbs = per * kp / (round_ms * 1e-3) / 1e9
+    return {"bytes_per_rhs_iter": round(per, 1), "nnz_stored": nnz_stored, "gbs": round(gbs, 1),
+            "frac": round(gbs / peak, 4)}
+
+
 def kernel_roofline(Bd, A, rounds=24, config="c2"):
     """Per-kernel CUDA-event timing of a PCG round at the bench's batch width,
     algorithmic bytes per launch, fraction of the HBM peak."""
@@ -183,7 +195,10 @@ def kernel_roofline(Bd, A, rounds=24, config="c2"):
                           "bytes": total_bytes,
                           "gbs": round(total_bytes / (total_ms * 1e-3) / 1e9, 1),
                           "frac": round(total_bytes / (total_ms * 1e-3) / 1e9 / peak, 4),
-                          "bytes_per_rhs_iter": total_bytes / kp},
+                          "bytes_per_rhs_iter": total_bytes / kp,
+                          # SURVEY.md §8(d)'s model of the reference recurrence (x, p, r, q
+                          # streamed every round; stored CSR incl. explicit zeros), for comparison
+                          "survey_model": survey_round(n, _nnz(A), kp, total_ms, peak)},
             "kernels": {k2: {kk: (round(v, 4) if isinstance(v, float) else v) for kk, v in d.items()}
                         for k2, d in kern.items()}}
 
