@@ -127,8 +127,10 @@ def survey_round(n, nnz_stored, kp, round_ms, peak):
     """bytes_per_rhs_iter(k) = 80 n + (12 nnz + 4 (n+1) + 16 n) / k."""
     per = 80 * n + (12 * nnz_stored + 4 * (n + 1) + 16 * n) / kp
     gbs = per * kp / (round_ms * 1e-3) / 1e9
-    return {"bytes_per_rhs_iter": round(per, 1), "nnz_stored": nnz_stored, "gbs": round(gbs, 1),
-            "frac": round(gbs / peak, 4)}
+    return {"bytes_per_rhs_iter": round(per, 1), "nnz_stored": nnz_stored, "equivalent_gbs": round(gbs, 1),
+            "equivalent_frac": round(gbs / peak, 4),
+            "note": "the model's bytes / the measured round time; above 1 because the round moves fewer bytes "
+                    "(x deferred over 8 rounds, explicit zeros pruned): see pcg_round.frac for the bytes moved"}
 
 
 def kernel_roofline(Bd, A, rounds=24, config="c2"):

@@ -370,27 +370,49 @@ __global__ void __launch_bounds__(Map<KP>::NT)
 // hf_pcg_stream runs more columns than the kp slots of a batch: a slot whose
 // column finished is harvested (its x and results copied out) and refilled with
 // the next column at a chunk boundary, so no slot idles while the slowest column
-// of a batch finishes.  k_refill is k_init restricted to the refilled slots
-// (slot[j] = source column, -2 = no column left: b = 0, state ZERO; -1 = keep):
-// the same per-row arithmetic and the same canonical b.b / b.z reductions, so a
-// column's iterates are bit-identical to a batch solve of it.
+// of a batch finishes.  One kernel does both, the slot lists passed by value (no
+// staging copy to wait for): harvest[j] = destination column of slot j's x, -1
+// none; refill[j] = source column, -2 = none (state ZERO; b = x = r = p = 0 on
+// the first fill), -1 = keep.
+// The refill is k_init restricted to the refilled slots: the same per-row
+// arithmetic and the same canonical b.b / b.z reductions, so a column's iterates
+// are bit-identical to a batch solve of it.
+struct SlotLists {
+  int refill[64];
+  int harvest[64];
+};
+
+struct Harvest {  // per-column results of hf_pcg_stream
+  double* X;      // n x ldb
+  int *iters, *state, *best_iter;
+  double *true_res, *best_res;
+};
+
 template <int KP>
 __global__ void __launch_bounds__(Map<KP>::NT)
-    k_refill(Ctl c, const int* __restrict__ slot_col, const double* __restrict__ Ball, int ldb,
-             double* Bs, const double* __restrict__ d, double* X, double* R, double* P, int init_dd) {
+    k_refill(Ctl c, const SlotLists sl, const double* __restrict__ Ball, int ldb, Harvest hv, double* Bs,
+             const double* __restrict__ d, double* X, double* R, double* P, int init_dd) {
   using M = Map<KP>;
   __shared__ double sm[M::RED];
   __shared__ double tot[2 * KP];
-  __shared__ int s_col[KP];
   const int tid = threadIdx.x, grp = tid / M::LPR, glane = tid % M::LPR;
-  for (int j = tid; j < KP; j += M::NT) s_col[j] = slot_col[j];
-  __syncthreads();
-  int col[M::CPL];
+  if (blockIdx.x == 0 && tid < KP && sl.harvest[tid] >= 0) {  // results, before the last block resets them
+    const int j = tid, col = sl.harvest[j];
+    hv.iters[col] = c.iters[j];
+    hv.state[col] = c.state[j];
+    hv.true_res[col] = c.true_res[j];
+    hv.best_res[col] = c.best_res[j];
+    hv.best_iter[col] = c.best_iter[j];
+  }
+  int col[M::CPL], hcol[M::CPL];
   bool any = false;
 #pragma unroll
   for (int k = 0; k < M::CPL; ++k) {
-    col[k] = s_col[glane * M::CPL + k];
-    any |= col[k] != -1;
+    col[k] = sl.refill[glane * M::CPL + k];
+    hcol[k] = sl.harvest[glane * M::CPL + k];
+    // b = 0 is written only by the first fill (empty slots of ncols < kp)
+    if (col[k] == -2 && !init_dd) col[k] = -3;
+    any |= col[k] != -1 || hcol[k] >= 0;
   }
   const int nt = n_tiles(c.n);
   double v[2][M::CPL];
@@ -405,7 +427,8 @@ __global__ void __launch_bounds__(Map<KP>::NT)
       if (init_dd && glane == 0) c.dd[row] = make_double2(dd, 1.0 / dd);
 #pragma unroll
       for (int k = 0; k < M::CPL; ++k) {
-        if (col[k] == -1) continue;
+        if (hcol[k] >= 0) hv.X[(size_t)row * ldb + hcol[k]] = X[o + k];
+        if (col[k] < 0 && col[k] != -2) continue;
         const double b = col[k] >= 0 ? Ball[(size_t)row * ldb + col[k]] : 0.0;
         const double z = __ddiv_rn(b, dd);
         v[0][k] = dot_acc(v[0][k], b, b);
@@ -423,7 +446,7 @@ __global__ void __launch_bounds__(Map<KP>::NT)
   if (tid < KP) {
     const int j = tid;
     st = c.state[j];
-    if (s_col[j] != -1) {
+    if (sl.refill[j] != -1) {
       const double nb = sqrt(tot[j]);
       c.normb[j] = nb;
       c.rz[j] = tot[KP + j];
@@ -438,29 +461,6 @@ __global__ void __launch_bounds__(Map<KP>::NT)
     }
   }
   census<KP>(c, st);
-}
-
-// Copy the finished slots' x into their columns of Xall and their results into
-// per-column arrays (slot_col[j] = destination column, -1 = none).
-template <int KP>
-__global__ void k_harvest(Ctl c, const int* __restrict__ slot_col, const double* __restrict__ X,
-                          double* Xall, int ldx, int* r_iters, int* r_state, double* r_true,
-                          double* r_best, int* r_best_it) {
-  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < KP) {
-    const int col = slot_col[t];
-    if (col >= 0) {
-      r_iters[col] = c.iters[t];
-      r_state[col] = c.state[t];
-      r_true[col] = c.true_res[t];
-      r_best[col] = c.best_res[t];
-      r_best_it[col] = c.best_iter[t];
-    }
-  }
-  if (t >= (size_t)c.n * KP) return;
-  const int row = (int)(t / KP), j = (int)(t % KP);
-  const int col = slot_col[j];
-  if (col >= 0) Xall[(size_t)row * ldx + col] = X[t];
 }
 
 // ---------------------------------------------------------------- SpMM over an ELL copy
@@ -1271,8 +1271,8 @@ inline int thread_resources(cudaStream_t* cap, int** hsum) {
     HF_CUDA(cudaStreamCreateWithFlags(&r.cap, cudaStreamNonBlocking));
     r.dev = dev;
   }
-  if (t_hsum == nullptr)
-    HF_CUDA(cudaHostAlloc(&t_hsum, sizeof(int) * SUM_N, cudaHostAllocPortable));
+  if (t_hsum == nullptr)  // summary words, then the per-slot states of hf_pcg_stream
+    HF_CUDA(cudaHostAlloc(&t_hsum, sizeof(int) * (SUM_N + 64), cudaHostAllocPortable));
   *cap = r.cap;
   *hsum = t_hsum;
   return HF_OK;
@@ -1375,10 +1375,10 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
 }
 
 // Column streaming (hf_pcg_stream): L >= 1 columns of Ball through kp slots.  The
-// host keeps LOOKAHEAD chunks queued; when a status read shows finished slots it
-// enqueues, behind the queued chunks, one harvest (x and results out) and one
-// refill (the next columns in, or b = 0 when none is left).  Terminal states never
-// change, so the queued chunks leave those slots alone until then.
+// host keeps one chunk (small systems: LOOKAHEAD) queued; when a status read shows
+// finished slots it enqueues, behind the queued chunks, one k_refill (their x and
+// results out, the next columns in, or b = 0 when none is left).  Terminal states
+// never change, so the queued chunks leave those slots alone until then.
 template <int KP>
 int run_stream(const hf_csr* A, const double* d, const double* Ball, int ldb, int ncols, int n,
                double tol, int max_iter, double* Xall, int32_t* iters, int32_t* status,
@@ -1389,13 +1389,13 @@ int run_stream(const hf_csr* A, const double* d, const double* Ball, int ldb, in
   Carve cv{reinterpret_cast<char*>(ws), L.bytes, ~size_t(0)};
   double* Bs = cv.take<double>((size_t)n * KP);  // the slots' right-hand sides (check path)
   double* X = cv.take<double>((size_t)n * KP);
-  int* d_refill = cv.take<int>(KP);
-  int* d_harvest = cv.take<int>(KP);
-  int* r_it = cv.take<int>(ncols);
-  int* r_st = cv.take<int>(ncols);
-  int* r_bi = cv.take<int>(ncols);
-  double* r_tr = cv.take<double>(ncols);
-  double* r_br = cv.take<double>(ncols);
+  Harvest hv;
+  hv.X = Xall;
+  hv.iters = cv.take<int>(ncols);
+  hv.state = cv.take<int>(ncols);
+  hv.best_iter = cv.take<int>(ncols);
+  hv.true_res = cv.take<double>(ncols);
+  hv.best_res = cv.take<double>(ncols);
   if (cv.used + 256 > ws_bytes) {
     set_error("pcg stream workspace too small: need %zu, have %zu", cv.used + 256, ws_bytes);
     return HF_ERR_WORKSPACE;
@@ -1405,10 +1405,8 @@ int run_stream(const hf_csr* A, const double* d, const double* Ball, int ldb, in
   cudaStream_t cap = nullptr;
   int* h_sum = nullptr;
   if (int rc = thread_resources(&cap, &h_sum)) return rc;
-  int* h_state = nullptr;  // per-slot states of the status read (pinned, freed on return)
-  HF_CUDA(cudaHostAlloc(&h_state, sizeof(int) * KP, cudaHostAllocPortable));
+  int* h_state = h_sum + SUM_N;  // per-slot states of the status read (pinned)
   struct Guard {
-    int* hs;
     cudaGraph_t g = nullptr;
     cudaGraphExec_t ge = nullptr;
     cudaEvent_t ev[LOOKAHEAD + 1] = {};
@@ -1417,27 +1415,25 @@ int run_stream(const hf_csr* A, const double* d, const double* Ball, int ldb, in
       if (g) cudaGraphDestroy(g);
       for (auto e : ev)
         if (e) cudaEventDestroy(e);
-      if (hs) cudaFreeHost(hs);
     }
-  } guard{h_state};
+  } guard;
   HF_CUDA(cudaMemsetAsync(L.counter, 0, sizeof(unsigned int) * 4, stream));
   HF_CUDA(cudaMemsetAsync(L.xmask, 0, sizeof(int) * (XD + 1) * KP, stream));
   HF_CUDA(cudaMemsetAsync(L.summary, 0, sizeof(int) * SUM_N, stream));
   HF_CUDA(cudaMemsetAsync(L.state, 0, sizeof(int) * KP, stream));
-  std::vector<int> slot_col(KP, -1), refill(KP), harvest(KP);
+  std::vector<int> slot_col(KP, -1);
+  SlotLists sl;
   int next = 0;
+  for (int j = 0; j < 64; ++j) sl.refill[j] = sl.harvest[j] = -1;
   for (int j = 0; j < KP; ++j) {
-    refill[j] = next < ncols ? next : -2;
-    slot_col[j] = refill[j] >= 0 ? refill[j] : -1;
+    sl.refill[j] = next < ncols ? next : -2;
+    slot_col[j] = sl.refill[j] >= 0 ? sl.refill[j] : -1;
     if (next < ncols) ++next;
   }
   auto enqueue_refill = [&](int init_dd) -> int {
-    HF_CUDA(cudaMemcpyAsync(d_refill, refill.data(), sizeof(int) * KP, cudaMemcpyHostToDevice, stream));
-    k_refill<KP><<<g.c.G, M::NT, 0, stream>>>(g.c, d_refill, Ball, ldb, Bs, d, X, L.R, L.P, init_dd);
+    k_refill<KP><<<g.c.G, M::NT, 0, stream>>>(g.c, sl, Ball, ldb, hv, Bs, d, X, L.R, L.P, init_dd);
     HF_LAUNCH_CHECK();
     count_launches(1);
-    // the staging array must not change before the copy ran
-    HF_CUDA(cudaStreamSynchronize(stream));
     return HF_OK;
   };
   if (int rc = enqueue_refill(1)) return rc;
@@ -1461,38 +1457,50 @@ int run_stream(const hf_csr* A, const double* d, const double* Ball, int ldb, in
   // A status read after chunk r may be newer but is never older; a slot refilled
   // behind chunk f is only trusted from the read of chunk f + 1 on.
   std::vector<long> fresh_from(KP, 0);
-  int harvested = 0;
+  // Chunks queued beyond the one whose status is read.  A finished slot idles
+  // until the read that sees it, so once a chunk outlasts the host's turnaround
+  // by far (n kp >= 4M values: ~0.5 ms and up) one chunk in flight is enough.
+  const int la = ((size_t)n * KP >= (size_t(1) << 22)) ? 1 : LOOKAHEAD;
+  // A finished slot with no column left to take is retired: it keeps its column
+  // (terminal states never change) until one harvest of all of them at the end.
+  std::vector<char> retired(KP, 0);
+  int harvested = 0;  // finished columns, harvested or retired
   long i = 0;
   for (; i < max_chunks && harvested < ncols; ++i) {
     HF_CUDA(cudaGraphLaunch(guard.ge, stream));
     count_launches(PER_CHUNK);
-    HF_CUDA(cudaEventRecord(guard.ev[i % (LOOKAHEAD + 1)], stream));
-    if (i < LOOKAHEAD) continue;
-    const long r = i - LOOKAHEAD;
-    HF_CUDA(cudaEventSynchronize(guard.ev[r % (LOOKAHEAD + 1)]));
+    HF_CUDA(cudaEventRecord(guard.ev[i % (la + 1)], stream));
+    if (i < la) continue;
+    const long r = i - la;
+    HF_CUDA(cudaEventSynchronize(guard.ev[r % (la + 1)]));
     bool any = false;
     for (int j = 0; j < KP; ++j) {
       const int st = ((volatile int*)h_state)[j];
       const bool done = st == S_DONE || st == S_FAILED || st == S_ZERO;
-      harvest[j] = (r >= fresh_from[j] && done && slot_col[j] >= 0) ? slot_col[j] : -1;
-      refill[j] = -1;
-      if (harvest[j] >= 0) {
+      const bool take = r >= fresh_from[j] && done && slot_col[j] >= 0 && !retired[j];
+      sl.harvest[j] = -1;
+      sl.refill[j] = -1;
+      if (!take) continue;
+      ++harvested;
+      if (next < ncols) {
         any = true;
-        ++harvested;
-        refill[j] = next < ncols ? next : -2;
-        slot_col[j] = next < ncols ? next : -1;
-        if (next < ncols) ++next;
+        sl.harvest[j] = slot_col[j];
+        sl.refill[j] = next;
+        slot_col[j] = next++;
         fresh_from[j] = i + 1;
+      } else {
+        retired[j] = 1;
       }
     }
-    if (!any) continue;
-    // behind the queued chunks: harvest, then refill
-    HF_CUDA(cudaMemcpyAsync(d_harvest, harvest.data(), sizeof(int) * KP, cudaMemcpyHostToDevice, stream));
-    const size_t work = (size_t)n * KP;
-    k_harvest<KP><<<(unsigned)((work + 255) / 256), 256, 0, stream>>>(g.c, d_harvest, X, Xall, ldb, r_it,
-                                                                      r_st, r_tr, r_br, r_bi);
-    HF_LAUNCH_CHECK();
-    count_launches(1);
+    // behind the queued chunks: harvest and refill in one pass
+    if (any)
+      if (int rc = enqueue_refill(0)) return rc;
+  }
+  if (harvested == ncols) {  // the retired slots' columns, in one pass
+    for (int j = 0; j < KP; ++j) {
+      sl.refill[j] = -1;
+      sl.harvest[j] = retired[j] ? slot_col[j] : -1;
+    }
     if (int rc = enqueue_refill(0)) return rc;
   }
   HF_CUDA(cudaStreamSynchronize(stream));
@@ -1500,11 +1508,11 @@ int run_stream(const hf_csr* A, const double* d, const double* Ball, int ldb, in
     set_error("pcg stream control did not finish: %d of %d columns after %ld chunks", harvested, ncols, i);
     return HF_ERR_INTERNAL;
   }
-  HF_CUDA(cudaMemcpyAsync(iters, r_it, sizeof(int) * ncols, cudaMemcpyDeviceToHost, stream));
-  HF_CUDA(cudaMemcpyAsync(status, r_st, sizeof(int) * ncols, cudaMemcpyDeviceToHost, stream));
-  HF_CUDA(cudaMemcpyAsync(true_res, r_tr, sizeof(double) * ncols, cudaMemcpyDeviceToHost, stream));
-  HF_CUDA(cudaMemcpyAsync(best_res, r_br, sizeof(double) * ncols, cudaMemcpyDeviceToHost, stream));
-  HF_CUDA(cudaMemcpyAsync(best_iter, r_bi, sizeof(int) * ncols, cudaMemcpyDeviceToHost, stream));
+  HF_CUDA(cudaMemcpyAsync(iters, hv.iters, sizeof(int) * ncols, cudaMemcpyDeviceToHost, stream));
+  HF_CUDA(cudaMemcpyAsync(status, hv.state, sizeof(int) * ncols, cudaMemcpyDeviceToHost, stream));
+  HF_CUDA(cudaMemcpyAsync(true_res, hv.true_res, sizeof(double) * ncols, cudaMemcpyDeviceToHost, stream));
+  HF_CUDA(cudaMemcpyAsync(best_res, hv.best_res, sizeof(double) * ncols, cudaMemcpyDeviceToHost, stream));
+  HF_CUDA(cudaMemcpyAsync(best_iter, hv.best_iter, sizeof(int) * ncols, cudaMemcpyDeviceToHost, stream));
   HF_CUDA(cudaStreamSynchronize(stream));
   return HF_OK;
 }
@@ -1514,8 +1522,6 @@ inline size_t stream_bytes(int n, int kp, int ncols) {
   Carve cv{nullptr, L.bytes, ~size_t(0)};
   cv.take<double>((size_t)n * kp);
   cv.take<double>((size_t)n * kp);
-  cv.take<int>(kp);
-  cv.take<int>(kp);
   for (int q = 0; q < 3; ++q) cv.take<int>(ncols);
   for (int q = 0; q < 2; ++q) cv.take<double>(ncols);
   return cv.used + 512;
