@@ -15,7 +15,7 @@ if [ "$what" = bench ]; then
   timeout 600 python tools/rank_share.py --config c5 --n 8 > $o/${tag}_c5_rank_share.jsonl 2>> $o/${tag}_rank_share.err
 else
   # everything is summarised here and the raw captures deleted: gpurun brings back <= 64 MiB
-  for cfg in c2 c4; do
+  for cfg in c2 c3 c4; do
     timeout 1200 ncu --profile-from-start off --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file $o/${tag}_${cfg}_launches.csv python tools/one_step.py --config $cfg > $o/${tag}_ncu_launch_$cfg.log 2>&1
     python tools/launch_shares.py $o/${tag}_${cfg}_launches.csv $o/${tag}_${cfg}_launch_shares.csv \
