@@ -219,6 +219,13 @@ def test_abi_rejects_bad_arguments_without_a_gpu():
     assert rc == 1 and b"kp=128" in L.hf_last_error()
     rc = L.hf_pcg_multi(C.byref(csr), 1, 1, 10, 4, 0.0, 10, P, 1, arr, arr, dbl, dbl, arr, 1, 0, P)
     assert rc == 1  # tol must be > 0 (PcgConfig's rule)
+    # hf_pcg_stream: null argument, ldb < ncols, unsupported kp
+    assert L.hf_pcg_stream(None, 1, 1, 8, 8, 10, 4, 1e-8, 10, 1, arr, arr, dbl, dbl, arr, 1, 0, P) == 1
+    assert b"null argument" in L.hf_last_error()
+    rc = L.hf_pcg_stream(C.byref(csr), 1, 1, 4, 8, 10, 4, 1e-8, 10, 1, arr, arr, dbl, dbl, arr, 1, 0, P)
+    assert rc == 1 and b"ldb=4" in L.hf_last_error()
+    rc = L.hf_pcg_stream(C.byref(csr), 1, 1, 8, 8, 10, 3, 1e-8, 10, 1, arr, arr, dbl, dbl, arr, 1, 0, P)
+    assert rc == 1 and b"kp=3" in L.hf_last_error()
     assert L.hf_ldp(None, P, P, None, P) == 1
     assert L.hf_eit_sens(P, P, P, P, 1, 0, P, 4, 4, P, 4, 2, P, P, 0, P) == 1
     assert L.hf_meg_rhs(P, P, P, 10, 10, 0, P, P, 600, P, 600, P, 0, P) == 1
@@ -231,6 +238,8 @@ def test_abi_workspace_queries_cover_new_entry_points():
     from paper_1811_07717_b200 import _native as N
 
     assert N.lib.hf_eit_sens_workspace_bytes(4_105_824) >= 4_105_824 * 16 * 8
+    # the stream workspace = a batch workspace's blocks + the slots' b and x + per-column results
+    assert N.lib.hf_pcg_stream_workspace_bytes(1000, 64, 300) > 2 * 1000 * 64 * 8 + 300 * 28
     assert N.lib.hf_meg_workspace_bytes(1000, 5800) > 5800 * 16 * 8
     assert N.lib.hf_ground_node_workspace_bytes(1000) >= 4 * 1002
     assert N.lib.hf_dof_partition_workspace_bytes(100_000) > 100_000 * 4
