@@ -67,7 +67,16 @@ def to_host(t, slot=7):
         stage = torch.from_numpy(buf[:nbytes].numpy().view(np.dtype(str(t.dtype).replace("torch.", ""))))
         stage = stage.view(t.shape)
         stage.copy_(t)  # synchronous device -> pinned copy
-        return stage.numpy().copy()
+        src = stage.numpy()
+        out = np.empty(src.shape, dtype=src.dtype)
+        flat_src, flat_dst = src.reshape(-1), out.reshape(-1)
+        pool = _pool()
+        step = -(-flat_src.size // (4 * _WORKERS))
+        futs = [pool.submit(np.copyto, flat_dst[i:i + step], flat_src[i:i + step])
+                for i in range(0, flat_src.size, step)]
+        for f in futs:
+            f.result()
+        return out
 
 
 def to_device(arr, dtype, dev=None, slot=0):

@@ -26,7 +26,7 @@ import scipy.sparse as sp
 import torch
 
 from . import _native as N
-from .device import DeviceCsr
+from .device import DeviceCsr, to_host
 from .errors import CurrentPatternError, DofError, SingularSystemError
 from .fem import DeviceMesh
 from .solver import PcgConfig, _raise_failed, operator, rhs_block, solve_block, transfer_device
@@ -213,7 +213,7 @@ def _electrode_response_device(sys, cfg):
 def electrode_response(sys, cfg=PcgConfig(), threads=1):
     """Transfer matrix T = A^-1 B and the symmetric response M = C - B'T (leadfield.py:104-109)."""
     _, T, M, _ = _electrode_response_device(sys, cfg)
-    return np.ascontiguousarray(T.cpu().numpy()), M
+    return to_host(T.contiguous()), M
 
 
 def lf_tail_device(T, Gt, W):
@@ -249,7 +249,7 @@ def eeg_leadfield(sys, cfg=PcgConfig(), threads=1):
     W = response_operator(M, sys.R)
     G = sys.G if sp.issparse(sys.G) else sp.csr_matrix(np.asarray(sys.G, dtype=float))
     Gt = DeviceCsr.from_scipy(sp.csr_matrix(G.T), T.device)
-    LF = lf_tail_device(T, Gt, W).cpu().numpy()
+    LF = to_host(lf_tail_device(T, Gt, W))
     src = sys.source_space
     return LeadField(matrix=LF, positions=src.positions if src is not None else None,
                      orientations=src.orientations if src is not None else None, modality="eeg")
@@ -345,7 +345,7 @@ def eit_leadfield(sys, dofs, currents, cfg=PcgConfig(), threads=1):
     U, info = solve_block(dsys.op, BV, cfg)
     _raise_failed(info, U, cfg, column_tag=False)  # pcg_solve semantics: no column tag
     cols = eit_columns_device(sys.mesh, dofs, sys.ground, T, U, response_operator(M, sys.R))
-    return LeadField(matrix=cols.cpu().numpy(), positions=dofs.centers, orientations=None,
+    return LeadField(matrix=to_host(cols.contiguous()), positions=dofs.centers, orientations=None,
                      modality="eit", n_patterns=P,
                      background_sigma=np.array(sys.mesh.sigma, copy=True),
                      background_data=y_bg.T.ravel())

@@ -28,6 +28,7 @@ import torch
 
 from . import _native as N
 from .device import device
+from .device import to_host as host_copy
 from .fem import DeviceMesh, assemble_device, blocks_device
 from .leadfield import LeadField, lf_tail_device
 from .solver import PcgConfig, _raise_failed, solve_block
@@ -137,7 +138,7 @@ class MegEngine:
         self.last_info = info
         ns = self.sensors.n_sensors
         L = self.primary() + lf_tail_device(T, self.Gt, -np.eye(ns))  # u = -A^-1 G q
-        return L.cpu().numpy() if to_host else L
+        return host_copy(L.contiguous()) if to_host else L
 
 
 def meg_leadfield(mesh, sensors, sources, cfg=PcgConfig()):

@@ -19,7 +19,7 @@ import scipy.sparse as sp
 import torch
 
 from . import _native as N
-from .device import DeviceCsr, PcgOperator, device, ldp_device, width_for
+from .device import DeviceCsr, PcgOperator, device, ldp_device, to_host, width_for
 from .errors import ConvergenceError, ParameterError, SingularPreconditionerError
 
 MAX_BATCH = 64  # RHS columns per multi-RHS solve (the widest kernel instantiation)
@@ -277,7 +277,7 @@ def transfer_matrix(A, B, cfg=PcgConfig(), threads=1):
     if not np.any(nonzero):
         return np.zeros((n, L))
     T, _ = transfer_device(A, B, cfg)
-    return np.ascontiguousarray(T.cpu().numpy())
+    return to_host(T.contiguous())
 
 
 __all__ = ["PcgConfig", "SolveInfo", "ldp", "pcg_solve", "transfer_matrix", "transfer_device",
