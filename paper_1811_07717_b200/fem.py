@@ -127,9 +127,16 @@ def volume_stiffness_device(mesh, sigma=None, elements=None):
     return assemble_device(dm, blocks, dm.n, tetra=sub)
 
 
+def _sorted(M):
+    """The assembled CSR has sorted column indices (scipy's COO -> CSR pattern, bit-exact):
+    record it so callers that check (`has_sorted_indices`, an O(nnz) scan) need not."""
+    M.has_sorted_indices = True
+    return M
+
+
 def volume_stiffness(mesh, sigma=None, elements=None):
     """Conductivity stiffness without electrode or grounding terms (fem.py:105-109)."""
-    return volume_stiffness_device(mesh, sigma, elements).to_scipy()
+    return _sorted(volume_stiffness_device(mesh, sigma, elements).to_scipy())
 
 
 def assemble_A_device(mesh, electrodes, ground=True):
@@ -152,7 +159,7 @@ def assemble_A_device(mesh, electrodes, ground=True):
 
 def assemble_A(mesh, electrodes, ground=True):
     """Grounded CEM stiffness matrix as scipy CSR (fem.py:197-224)."""
-    return assemble_A_device(mesh, electrodes, ground)[0].to_scipy()
+    return _sorted(assemble_A_device(mesh, electrodes, ground)[0].to_scipy())
 
 
 __all__ = ["stiffness_blocks", "volume_stiffness", "assemble_A", "assemble_A_device",
