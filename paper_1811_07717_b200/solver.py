@@ -149,8 +149,10 @@ def _solve_streamed(op, B, cfg, kp, max_iter, X, info):
     failed columns are replayed to their best iterate in batches."""
     n, k = B.shape
     Bc = B if B.is_contiguous() else B.contiguous()
-    if not X.is_contiguous():
-        raise ValueError("output block must be contiguous")
+    if not X.is_contiguous():  # a strided `out`: solve into a dense block, then copy
+        Xd, info = _solve_streamed(op, Bc, cfg, kp, max_iter, torch.empty_like(Bc), info)
+        X.copy_(Xd)
+        return X, info
     ws = torch.empty(N.lib.hf_pcg_stream_workspace_bytes(n, kp, k), dtype=torch.uint8, device=B.device)
     it = np.zeros(k, dtype=np.int32)
     stt = np.zeros(k, dtype=np.int32)
