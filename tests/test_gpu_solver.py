@@ -355,6 +355,23 @@ class TestStream:
         assert 0 < fails < 30
         self._same(self._solve(A, B, cfg, 4), ref)
 
+    def test_stream_into_strided_output(self, eng):
+        import torch
+
+        from paper_1811_07717_b200.solver import operator, rhs_block, solve_block
+        from tests.fixtures import csr
+
+        fx = load("layered_h12.npz")
+        A, B = csr(fx, "A"), csr(fx, "B").toarray()
+        cfg = eng.PcgConfig(tolerance=1e-10)
+        Bd = rhs_block(B)
+        big = torch.full((Bd.shape[0], 2 * Bd.shape[1]), float("nan"), dtype=torch.float64, device=Bd.device)
+        out = big[:, ::2]                                   # strided view
+        X, _ = solve_block(operator(A, cfg), Bd, cfg, batch=4, out=out)
+        assert X.data_ptr() == out.data_ptr()
+        ref, _ = solve_block(operator(A, cfg), Bd, cfg, batch=64)
+        assert torch.equal(out, ref) and torch.isnan(big[:, 1::2]).all()
+
     def test_stream_fewer_columns_than_slots(self, eng):
         from paper_1811_07717_b200.solver import _solve_streamed, operator, rhs_block, SolveInfo
         from tests.fixtures import csr
