@@ -463,6 +463,126 @@ __global__ void __launch_bounds__(Map<KP>::NT)
   census<KP>(c, st);
 }
 
+// Device-side slot scheduler of hf_pcg_stream, the last node of every captured
+// chunk (after the check path, so DONE / FAILED are final): every block derives
+// the same decisions from the slot states, then it is k_refill with those lists.
+// A finished slot takes the next column (slot order), or retires when none is
+// left; its results go out now, a retired slot's x at the final harvest.
+struct Sched {
+  int* slot_col;  // column in each slot, -1 = none
+  int* retired;   // 1 = finished, nothing left to take, x not yet harvested
+  int* next;      // next column to hand out
+  int* nfin;      // finished columns (harvested or retired); the host stops at ncols
+  int ncols;
+};
+
+template <int KP>
+__global__ void __launch_bounds__(Map<KP>::NT)
+    k_sched(Ctl c, Sched sc, const double* __restrict__ Ball, int ldb, Harvest hv, double* Bs,
+            const double* __restrict__ d, double* X, double* R, double* P) {
+  using M = Map<KP>;
+  __shared__ double sm[M::RED];
+  __shared__ double tot[2 * KP];
+  __shared__ int s_take[KP], s_ref[KP], s_harv[KP];
+  const int tid = threadIdx.x, grp = tid / M::LPR, glane = tid % M::LPR;
+  const int nx = *sc.next;
+  int take = 0;
+  if (tid < KP) {
+    const int st = c.state[tid];
+    take = (st == S_DONE || st == S_FAILED || st == S_ZERO) && sc.slot_col[tid] >= 0 && !sc.retired[tid];
+    s_take[tid] = take;
+  }
+  const int ntake = __syncthreads_count(take);
+  if (ntake == 0) return;  // the common case: nothing finished in this chunk
+  int refill = 0;
+  if (tid < KP) {
+    int rank = 0;
+    for (int i = 0; i < tid; ++i) rank += s_take[i];
+    const int col = nx + rank;
+    s_ref[tid] = (take && col < sc.ncols) ? col : -1;
+    s_harv[tid] = (take && col < sc.ncols) ? sc.slot_col[tid] : -1;
+    refill = s_ref[tid] >= 0;
+  }
+  const int nref = __syncthreads_count(refill);
+  if (blockIdx.x == 0 && tid < KP && s_take[tid]) {  // results, before the last block resets them
+    const int j = tid, col = sc.slot_col[j];
+    hv.iters[col] = c.iters[j];
+    hv.state[col] = c.state[j];
+    hv.true_res[col] = c.true_res[j];
+    hv.best_res[col] = c.best_res[j];
+    hv.best_iter[col] = c.best_iter[j];
+  }
+  if (nref == 0) {  // no column left (every block sees it): block 0 retires the slots
+    if (blockIdx.x == 0) {
+      __syncthreads();
+      if (tid < KP && s_take[tid]) sc.retired[tid] = 1;
+      if (tid == 0) *sc.nfin += ntake;
+    }
+    return;
+  }
+  int col[M::CPL], hcol[M::CPL];
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) {
+    col[k] = s_ref[glane * M::CPL + k];
+    hcol[k] = s_harv[glane * M::CPL + k];
+    any |= col[k] >= 0;
+  }
+  const int nt = n_tiles(c.n);
+  double v[2][M::CPL];
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) v[0][k] = v[1][k] = 0.0;
+  if (any) {
+    for (int t = blockIdx.x; t < nt; t += c.G) {
+      const int row = t * TR + grp;
+      if (row >= c.n) continue;
+      const size_t o = (size_t)row * KP + glane * M::CPL;
+      const double dd = d[row];
+#pragma unroll
+      for (int k = 0; k < M::CPL; ++k) {
+        if (col[k] < 0) continue;
+        hv.X[(size_t)row * ldb + hcol[k]] = X[o + k];
+        const double b = Ball[(size_t)row * ldb + col[k]];
+        const double z = __ddiv_rn(b, dd);
+        v[0][k] = dot_acc(v[0][k], b, b);
+        v[1][k] = dot_acc(v[1][k], b, z);
+        Bs[o + k] = b;
+        X[o + k] = 0.0;
+        R[o + k] = b;
+        P[o + k] = z;
+      }
+    }
+  }
+  block_partials<M, 2>(v, sm, c);
+  if (!last_block_reduce<M, 2>(c, sm, tot)) return;
+  int st = -1;
+  if (tid < KP) {
+    const int j = tid;
+    st = c.state[j];
+    if (s_ref[j] >= 0) {
+      const double nb = sqrt(tot[j]);
+      c.normb[j] = nb;
+      c.rz[j] = tot[KP + j];
+      c.beta[j] = 0.0;
+      c.best_res[j] = 1.0;
+      c.best_iter[j] = 0;
+      c.iters[j] = 0;
+      c.true_res[j] = 0.0;
+      c.pmask[j] = 0;
+      st = nb == 0.0 ? S_ZERO : S_RUN;
+      c.state[j] = st;
+      sc.slot_col[j] = s_ref[j];
+    } else if (s_take[j]) {
+      sc.retired[j] = 1;
+    }
+  }
+  if (tid == 0) {
+    *sc.next = nx + nref;
+    *sc.nfin += ntake;
+  }
+  census<KP>(c, st);
+}
+
 // ---------------------------------------------------------------- SpMM over an ELL copy
 // The SpMM runs on a padded ELL copy of the zero-free matrix (8 slots per row,
 // built once per solve by k_ell_fill).  Empty slots 0..ELL_OPT-1 hold (row
@@ -1375,10 +1495,10 @@ int run(const hf_csr* A, const double* d, const double* B, int n, double tol, in
 }
 
 // Column streaming (hf_pcg_stream): L >= 1 columns of Ball through kp slots.  The
-// host keeps one chunk (small systems: LOOKAHEAD) queued; when a status read shows
-// finished slots it enqueues, behind the queued chunks, one k_refill (their x and
-// results out, the next columns in, or b = 0 when none is left).  Terminal states
-// never change, so the queued chunks leave those slots alone until then.
+// slots are scheduled on the device (k_sched ends every chunk), so a finished slot
+// takes its next column at the end of the chunk it finished in; the host only
+// keeps LOOKAHEAD chunks queued and stops once every column is finished, then
+// harvests the retired slots' x in one pass.
 template <int KP>
 int run_stream(const hf_csr* A, const double* d, const double* Ball, int ldb, int ncols, int n,
                double tol, int max_iter, double* Xall, int32_t* iters, int32_t* status,
@@ -1396,6 +1516,12 @@ int run_stream(const hf_csr* A, const double* d, const double* Ball, int ldb, in
   hv.best_iter = cv.take<int>(ncols);
   hv.true_res = cv.take<double>(ncols);
   hv.best_res = cv.take<double>(ncols);
+  Sched sched;
+  sched.slot_col = cv.take<int>(2 * KP + 2);  // slot_col, retired, next, nfin: one block
+  sched.retired = sched.slot_col + KP;
+  sched.next = sched.slot_col + 2 * KP;
+  sched.nfin = sched.next + 1;
+  sched.ncols = ncols;
   if (cv.used + 256 > ws_bytes) {
     set_error("pcg stream workspace too small: need %zu, have %zu", cv.used + 256, ws_bytes);
     return HF_ERR_WORKSPACE;
@@ -1405,7 +1531,7 @@ int run_stream(const hf_csr* A, const double* d, const double* Ball, int ldb, in
   cudaStream_t cap = nullptr;
   int* h_sum = nullptr;
   if (int rc = thread_resources(&cap, &h_sum)) return rc;
-  int* h_state = h_sum + SUM_N;  // per-slot states of the status read (pinned)
+  int* h_nfin = h_sum + SUM_N;  // finished-column count of the status read (pinned)
   struct Guard {
     cudaGraph_t g = nullptr;
     cudaGraphExec_t ge = nullptr;
@@ -1421,27 +1547,25 @@ int run_stream(const hf_csr* A, const double* d, const double* Ball, int ldb, in
   HF_CUDA(cudaMemsetAsync(L.xmask, 0, sizeof(int) * (XD + 1) * KP, stream));
   HF_CUDA(cudaMemsetAsync(L.summary, 0, sizeof(int) * SUM_N, stream));
   HF_CUDA(cudaMemsetAsync(L.state, 0, sizeof(int) * KP, stream));
-  std::vector<int> slot_col(KP, -1);
+  // first fill: slot j <- column j (b = 0 and state ZERO for slots beyond ncols)
   SlotLists sl;
-  int next = 0;
+  std::vector<int> ctl(2 * KP + 2, 0);  // slot_col, retired, next, nfin
   for (int j = 0; j < 64; ++j) sl.refill[j] = sl.harvest[j] = -1;
   for (int j = 0; j < KP; ++j) {
-    sl.refill[j] = next < ncols ? next : -2;
-    slot_col[j] = sl.refill[j] >= 0 ? sl.refill[j] : -1;
-    if (next < ncols) ++next;
+    sl.refill[j] = j < ncols ? j : -2;
+    ctl[j] = j < ncols ? j : -1;
   }
-  auto enqueue_refill = [&](int init_dd) -> int {
-    k_refill<KP><<<g.c.G, M::NT, 0, stream>>>(g.c, sl, Ball, ldb, hv, Bs, d, X, L.R, L.P, init_dd);
-    HF_LAUNCH_CHECK();
-    count_launches(1);
-    return HF_OK;
-  };
-  if (int rc = enqueue_refill(1)) return rc;
+  ctl[2 * KP] = std::min(KP, ncols);
+  HF_CUDA(cudaMemcpyAsync(sched.slot_col, ctl.data(), sizeof(int) * ctl.size(), cudaMemcpyHostToDevice, stream));
+  k_refill<KP><<<g.c.G, M::NT, 0, stream>>>(g.c, sl, Ball, ldb, hv, Bs, d, X, L.R, L.P, 1);
+  HF_LAUNCH_CHECK();
+  count_launches(1);
   HF_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
   for (int r = 0; r < CHUNK; ++r) launch_round<KP>(g, L, X, r, cap, nullptr);
   launch_check<KP>(g, L, Bs, X, cap);
+  k_sched<KP><<<g.c.G, M::NT, 0, cap>>>(g.c, sched, Ball, ldb, hv, Bs, d, X, L.R, L.P);
   cudaMemcpyAsync(h_sum, L.summary, sizeof(int) * SUM_N, cudaMemcpyDeviceToHost, cap);
-  cudaMemcpyAsync(h_state, L.state, sizeof(int) * KP, cudaMemcpyDeviceToHost, cap);
+  cudaMemcpyAsync(h_nfin, sched.nfin, sizeof(int), cudaMemcpyDeviceToHost, cap);
   const cudaError_t le = cudaGetLastError();
   const cudaError_t ce = cudaStreamEndCapture(cap, &guard.g);
   if (ce != cudaSuccess || le != cudaSuccess) {
@@ -1450,64 +1574,36 @@ int run_stream(const hf_csr* A, const double* d, const double* Ball, int ldb, in
   }
   HF_CUDA(cudaGraphInstantiate(&guard.ge, guard.g, 0));
   for (auto& e : guard.ev) HF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-  // every column needs at most max_iter + 1 chunks in its slot and waits at most
-  // LOOKAHEAD + 1 chunks for a refill
+  // every column needs at most max_iter + 1 chunks in its slot and takes its slot
+  // at the end of the chunk its predecessor finished in
   const long per_col = (long)max_iter + 2 * LOOKAHEAD + 8;
   const long max_chunks = per_col * ((ncols + KP - 1) / KP + 1);
-  // A status read after chunk r may be newer but is never older; a slot refilled
-  // behind chunk f is only trusted from the read of chunk f + 1 on.
-  std::vector<long> fresh_from(KP, 0);
-  // Chunks queued beyond the one whose status is read.  A finished slot idles
-  // until the read that sees it, so once a chunk outlasts the host's turnaround
-  // by far (n kp >= 4M values: ~0.5 ms and up) one chunk in flight is enough.
-  const int la = ((size_t)n * KP >= (size_t(1) << 22)) ? 1 : LOOKAHEAD;
-  // A finished slot with no column left to take is retired: it keeps its column
-  // (terminal states never change) until one harvest of all of them at the end.
-  std::vector<char> retired(KP, 0);
-  int harvested = 0;  // finished columns, harvested or retired
+  int nfin = 0;
   long i = 0;
-  for (; i < max_chunks && harvested < ncols; ++i) {
+  for (; i < max_chunks && nfin < ncols; ++i) {
     HF_CUDA(cudaGraphLaunch(guard.ge, stream));
-    count_launches(PER_CHUNK);
-    HF_CUDA(cudaEventRecord(guard.ev[i % (la + 1)], stream));
-    if (i < la) continue;
-    const long r = i - la;
-    HF_CUDA(cudaEventSynchronize(guard.ev[r % (la + 1)]));
-    bool any = false;
-    for (int j = 0; j < KP; ++j) {
-      const int st = ((volatile int*)h_state)[j];
-      const bool done = st == S_DONE || st == S_FAILED || st == S_ZERO;
-      const bool take = r >= fresh_from[j] && done && slot_col[j] >= 0 && !retired[j];
-      sl.harvest[j] = -1;
-      sl.refill[j] = -1;
-      if (!take) continue;
-      ++harvested;
-      if (next < ncols) {
-        any = true;
-        sl.harvest[j] = slot_col[j];
-        sl.refill[j] = next;
-        slot_col[j] = next++;
-        fresh_from[j] = i + 1;
-      } else {
-        retired[j] = 1;
-      }
-    }
-    // behind the queued chunks: harvest and refill in one pass
-    if (any)
-      if (int rc = enqueue_refill(0)) return rc;
-  }
-  if (harvested == ncols) {  // the retired slots' columns, in one pass
-    for (int j = 0; j < KP; ++j) {
-      sl.refill[j] = -1;
-      sl.harvest[j] = retired[j] ? slot_col[j] : -1;
-    }
-    if (int rc = enqueue_refill(0)) return rc;
+    count_launches(PER_CHUNK + 1);
+    HF_CUDA(cudaEventRecord(guard.ev[i % (LOOKAHEAD + 1)], stream));
+    if (i < LOOKAHEAD) continue;
+    HF_CUDA(cudaEventSynchronize(guard.ev[(i - LOOKAHEAD) % (LOOKAHEAD + 1)]));
+    nfin = *(volatile int*)h_nfin;
   }
   HF_CUDA(cudaStreamSynchronize(stream));
-  if (harvested < ncols) {
-    set_error("pcg stream control did not finish: %d of %d columns after %ld chunks", harvested, ncols, i);
+  nfin = *(volatile int*)h_nfin;
+  if (nfin < ncols) {
+    set_error("pcg stream control did not finish: %d of %d columns after %ld chunks", nfin, ncols, i);
     return HF_ERR_INTERNAL;
   }
+  // the retired slots' x, in one pass
+  HF_CUDA(cudaMemcpyAsync(ctl.data(), sched.slot_col, sizeof(int) * 2 * KP, cudaMemcpyDeviceToHost, stream));
+  HF_CUDA(cudaStreamSynchronize(stream));
+  for (int j = 0; j < KP; ++j) {
+    sl.refill[j] = -1;
+    sl.harvest[j] = ctl[KP + j] ? ctl[j] : -1;
+  }
+  k_refill<KP><<<g.c.G, M::NT, 0, stream>>>(g.c, sl, Ball, ldb, hv, Bs, d, X, L.R, L.P, 0);
+  HF_LAUNCH_CHECK();
+  count_launches(1);
   HF_CUDA(cudaMemcpyAsync(iters, hv.iters, sizeof(int) * ncols, cudaMemcpyDeviceToHost, stream));
   HF_CUDA(cudaMemcpyAsync(status, hv.state, sizeof(int) * ncols, cudaMemcpyDeviceToHost, stream));
   HF_CUDA(cudaMemcpyAsync(true_res, hv.true_res, sizeof(double) * ncols, cudaMemcpyDeviceToHost, stream));
@@ -1524,6 +1620,7 @@ inline size_t stream_bytes(int n, int kp, int ncols) {
   cv.take<double>((size_t)n * kp);
   for (int q = 0; q < 3; ++q) cv.take<int>(ncols);
   for (int q = 0; q < 2; ++q) cv.take<double>(ncols);
+  cv.take<int>(2 * kp + 2);
   return cv.used + 512;
 }
 
