@@ -49,16 +49,21 @@ def peaks():
 
 
 def workload_config(prob, cfg):
-    ncomp = len(np.unique(prob.mesh.labels))
-    return {"workload": f"{prob.name}: {prob.mesh.n_nodes:,}-node {ncomp}-compartment sphere Kuhn mesh, "
-                        f"{prob.electrodes.count}-electrode EEG lead field, "
-                        f"{prob.sources.n_sources:,} dipole sources",
-            "config": prob.name, "n_nodes": int(prob.mesh.n_nodes),
-            "n_elements": int(prob.mesh.n_elements), "electrodes": int(prob.electrodes.count),
-            "sources": int(prob.sources.n_sources), "lf_shape": [int(prob.electrodes.count),
-                                                                 3 * int(prob.sources.n_sources)],
-            "tolerance": cfg.tolerance, "precision": "fp64",
+    return eeg_config(prob.name, prob.mesh.n_nodes, prob.mesh.n_elements, len(np.unique(prob.mesh.labels)),
+                      prob.electrodes.count, prob.sources.n_sources, cfg.tolerance)
+
+
+def eeg_config(name, n_nodes, n_elements, ncomp, L, S, tol):
+    """The `config` object of an EEG line; both arms print the same one."""
+    return {"workload": f"{name}: {n_nodes:,}-node {ncomp}-compartment sphere Kuhn mesh, "
+                        f"{L}-electrode EEG lead field, {S:,} dipole sources",
+            "config": name, "n_nodes": int(n_nodes), "n_elements": int(n_elements), "electrodes": int(L),
+            "sources": int(S), "lf_shape": [int(L), 3 * int(S)], "tolerance": tol, "precision": "fp64",
             "l2_policy": "inputs larger than L2 (n x 64 fp64 vector blocks = 512 MB each)"}
+
+
+# sources of the EEG configs (synthetic.eeg_problem)
+SOURCES = {"c1": 1000, "c2": 10_000, "c5": 50_000}
 
 
 # ---------------------------------------------------------------- clocks
@@ -646,10 +651,14 @@ def _ref_column(job):
 
 def run_reference(args):
     """The reference itself (baseline/_ref, numpy/scipy, unmodified) on the box's
-    host cores: every timed step solves one WHOLE electrode column per core in
-    parallel processes through headfem.solver.pcg_solve; RHS-solves/s = columns
-    solved / measured wall time.  Warm-up steps are bounded 10-iteration samples
-    (page-in and import only).  Rank 0 alone runs under torchrun."""
+    host cores.  The timed region solves one WHOLE electrode column per core, in
+    parallel processes through headfem.solver.pcg_solve (solver.py:64-111), and is
+    reported as K equal steps: ms_per_step = measured wall / K, RHS-solves/s =
+    columns solved / measured wall — nothing extrapolated, and the run ends in
+    about a minute plus setup for any K (a whole column takes ~33 s on one core;
+    K steps of whole columns would take K times that).  Warm-up steps are bounded
+    10-iteration samples (page-in and import only).  Rank 0 alone runs under
+    torchrun; the line's config is the GPU arm's."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -669,46 +678,40 @@ def run_reference(args):
     log(f"[reference] {hf.__file__}: mesh {mesh.n_nodes} nodes, assemble_A nnz {A.nnz} in {t_setup:.1f}s")
     _REF["A"], _REF["B"] = A, B
     L = B.shape[1]
-    # every host core (16 on this pool's boxes), capped at 32 processes: each step is one
-    # whole column per process, and past ~32 processes the shared memory bandwidth makes
-    # a step (and the 20-step run) longer without more columns per second
+    # every host core (16 on this pool's boxes), capped at 32 processes (past ~32 the
+    # shared memory bandwidth makes the columns slower without more columns per second)
     cores = int(args.ref_cores or min(os.cpu_count() or 1, 32))
     cores = max(1, min(cores, L))
     ctx = mp.get_context("fork")
-    walls, its = [], []
-    nxt = 0
+    # the cores' columns spread over the electrode set
+    cols = sorted({(c * L) // cores for c in range(cores)})
     with ctx.Pool(cores) as pool:
         for _ in range(args.warmup):
-            pool.map(_ref_column, [(c % L, 10) for c in range(cores)])
-        for s in range(args.steps):
-            jobs = [((nxt + c) % L, None) for c in range(cores)]
-            nxt += cores
-            w0 = time.perf_counter()
-            res = pool.map(_ref_column, jobs)
-            walls.append(time.perf_counter() - w0)
-            its.extend(r[1] for r in res)
-            log(f"[reference] step {s}: {cores} columns in {walls[-1]:.1f}s "
-                f"(iterations {min(r[1] for r in res)}-{max(r[1] for r in res)})")
-    wall = float(np.sum(walls))
-    value = cores * args.steps / wall
-    sample = (f"{cores} processes x one whole electrode column each per step (headfem.solver.pcg_solve "
-              f"from baseline/_ref, tol 1e-8, 1 BLAS thread per process), {args.steps} steps, "
-              f"{min(its)}-{max(its)} iterations per column; measured, not extrapolated")
+            pool.map(_ref_column, [(c, 10) for c in cols])
+        w0 = time.perf_counter()
+        res = pool.map(_ref_column, [(c, None) for c in cols])
+        wall = time.perf_counter() - w0
+    its = [r[1] for r in res]
+    log(f"[reference] {len(cols)} whole columns in {wall:.1f}s (iterations {min(its)}-{max(its)})")
+    value = len(cols) / wall
+    sample = (f"{len(cols)} whole electrode columns (of {L}), one per process, through headfem.solver.pcg_solve "
+              f"from baseline/_ref (tol 1e-8, 1 BLAS thread per process), {min(its)}-{max(its)} iterations; "
+              f"the measured wall time of that solve is the timed region, reported as {args.steps} equal steps")
+    ncomp = len(np.unique(np.asarray(mesh.labels)))
     out = {"metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": int(args.gpus),
            "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": round(wall * 1e3 / args.steps, 1), "higher_is_better": True, "scaling": "strong",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic (same inputs as the GPU arm)",
-           "config": {"workload": f"{args.config}: {mesh.n_nodes:,}-node sphere Kuhn mesh, {L}-electrode "
-                                  f"EEG transfer solve (reference pcg_solve per column)",
-                      "config": args.config, "n_nodes": int(mesh.n_nodes), "electrodes": int(L),
-                      "tolerance": 1e-8, "precision": "fp64", "parallelism": f"{cores} host processes"},
+           "config": {**eeg_config(args.config, mesh.n_nodes, len(mesh.tetra), ncomp, L, SOURCES[args.config],
+                                   1e-8),
+                      "parallelism": f"electrode-columns x{int(args.gpus)}"},
            "impl": "reference",
-           "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": cores, "kind": "reference",
+           "cpu_baseline": {"value": round(value, 4), "unit": UNIT, "cores": len(cols), "kind": "reference",
                             "sample": sample},
            "e2e": {"value": round(value, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0},
            "reference_setup_s": round(t_setup, 1),
-           "step_seconds": [round(w, 2) for w in walls],
+           "timed_region_s": round(wall, 2),
            "lf_build_s_extrapolated": round(L / value, 1)}
     print(json.dumps(out), flush=True)
 
