@@ -476,6 +476,114 @@ struct Sched {
   int ncols;
 };
 
+// Tail compaction.  Once no column is left to hand out, finished slots leave
+// holes and the kernels keep moving every lane that still holds a running
+// column; when the running columns would fit in at least two fewer 4-slot lane
+// groups, one pass harvests every finished slot's x and moves the running
+// columns from the high slots into the lowest free ones (x, r, b and the p in
+// ring slot 0 — where a running column's p is at a chunk end — plus its control
+// words), so lanes above them go idle.  A column's arithmetic does not depend
+// on its slot (canonical reductions), so its results stay bit-identical.
+// Returns false (nothing done, no block touched anything) when not worth it.
+template <int KP>
+__device__ bool compact_tail(Ctl& c, Sched& sc, int ntake, const int* s_take, int* s_harv, int* s_src,
+                             int ldb, Harvest& hv, double* Bs, double* X, double* R, double* P, double* sm,
+                             double* tot) {
+  using M = Map<KP>;
+  __shared__ int s_go;
+  const int tid = threadIdx.x, grp = tid / M::LPR, glane = tid % M::LPR;
+  if (tid == 0) {
+    int m = 0, groups = 0, gmask = 0;
+    int active[KP];
+    for (int j = 0; j < KP; ++j) {
+      active[j] = sc.slot_col[j] >= 0 && !sc.retired[j] && !s_take[j];
+      m += active[j];
+      if (active[j]) gmask |= 1 << (j / 4);
+    }
+    for (int q = 0; q < KP / 4; ++q) groups += (gmask >> q) & 1;
+    s_go = m > 0 && groups - (m + 3) / 4 >= 2;
+    if (s_go) {
+      int src = m;
+      for (int j = 0; j < KP; ++j) {
+        s_harv[j] = (sc.slot_col[j] >= 0 && !active[j]) ? sc.slot_col[j] : -1;  // finished: x out
+        s_src[j] = -1;
+      }
+      for (int f = 0; f < m; ++f) {
+        if (active[f]) continue;
+        while (!active[src]) ++src;
+        s_src[f] = src++;
+      }
+    }
+  }
+  __syncthreads();
+  if (!s_go) return false;
+  const size_t nk = (size_t)c.n * KP;
+  int hcol[M::CPL], from[M::CPL];
+  bool any = false;
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) {
+    hcol[k] = s_harv[glane * M::CPL + k];
+    from[k] = s_src[glane * M::CPL + k];
+    any |= hcol[k] >= 0 || from[k] >= 0;
+  }
+  if (any) {
+    const int nt = n_tiles(c.n);
+    for (int t = blockIdx.x; t < nt; t += c.G) {
+      const int row = t * TR + grp;
+      if (row >= c.n) continue;
+      const size_t o = (size_t)row * KP + glane * M::CPL, r0 = (size_t)row * KP;
+#pragma unroll
+      for (int k = 0; k < M::CPL; ++k) {
+        if (hcol[k] >= 0) hv.X[(size_t)row * ldb + hcol[k]] = X[o + k];
+        if (from[k] < 0) continue;
+        X[o + k] = X[r0 + from[k]];
+        R[o + k] = R[r0 + from[k]];
+        Bs[o + k] = Bs[r0 + from[k]];
+        P[o + k] = P[r0 + from[k]];  // ring slot 0
+      }
+    }
+  }
+  // no reduction: the partials only carry the last-block election
+  double v[1][M::CPL];
+#pragma unroll
+  for (int k = 0; k < M::CPL; ++k) v[0][k] = 0.0;
+  block_partials<M, 1>(v, sm, c);
+  if (!last_block_reduce<M, 1>(c, sm, tot)) return true;
+  __syncthreads();
+  if (tid == 0) {
+    for (int f = 0; f < KP; ++f) {
+      if (s_harv[f] >= 0) {  // harvested: the slot is empty
+        sc.slot_col[f] = -1;
+        sc.retired[f] = 0;
+        c.state[f] = S_ZERO;
+      }
+    }
+    for (int f = 0; f < KP; ++f) {
+      const int a = s_src[f];
+      if (a < 0) continue;
+      c.state[f] = c.state[a];
+      c.normb[f] = c.normb[a];
+      c.rz[f] = c.rz[a];
+      c.beta[f] = c.beta[a];
+      c.best_res[f] = c.best_res[a];
+      c.best_iter[f] = c.best_iter[a];
+      c.iters[f] = c.iters[a];
+      c.true_res[f] = c.true_res[a];
+      c.pmask[f] = c.pmask[a];
+      c.pbuf[f] = c.pbuf[a];
+      sc.slot_col[f] = sc.slot_col[a];
+      sc.retired[f] = 0;
+      sc.slot_col[a] = -1;
+      sc.retired[a] = 0;
+      c.state[a] = S_ZERO;
+    }
+    *sc.nfin += ntake;
+  }
+  __syncthreads();
+  census<KP>(c, tid < KP ? c.state[tid] : -1);
+  return true;
+}
+
 template <int KP>
 __global__ void __launch_bounds__(Map<KP>::NT)
     k_sched(Ctl c, Sched sc, const double* __restrict__ Ball, int ldb, Harvest hv, double* Bs,
@@ -512,8 +620,9 @@ __global__ void __launch_bounds__(Map<KP>::NT)
     hv.best_res[col] = c.best_res[j];
     hv.best_iter[col] = c.best_iter[j];
   }
-  if (nref == 0) {  // no column left (every block sees it): block 0 retires the slots
-    if (blockIdx.x == 0) {
+  if (nref == 0) {  // no column left (every block sees it)
+    if (compact_tail<KP>(c, sc, ntake, s_take, s_harv, s_ref, ldb, hv, Bs, X, R, P, sm, tot)) return;
+    if (blockIdx.x == 0) {  // block 0 retires the finished slots
       __syncthreads();
       if (tid < KP && s_take[tid]) sc.retired[tid] = 1;
       if (tid == 0) *sc.nfin += ntake;
