@@ -517,7 +517,6 @@ __device__ bool compact_tail(Ctl& c, Sched& sc, int ntake, const int* s_take, in
   }
   __syncthreads();
   if (!s_go) return false;
-  const size_t nk = (size_t)c.n * KP;
   int hcol[M::CPL], from[M::CPL];
   bool any = false;
 #pragma unroll
