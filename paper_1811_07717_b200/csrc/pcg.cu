@@ -55,6 +55,8 @@ constexpr int RSEG = 8;       // segments of the last-block reduction
 constexpr int CHUNK = 8;      // PCG rounds per captured graph
 constexpr int LOOKAHEAD = 3;  // chunks queued beyond the one whose status is read
 constexpr int ELL_W = 8;      // slots per row of the ELL copy of A
+constexpr int ELL_LONG = 1 << 30;  // slot 0 flag: the row has entries beyond the slots
+constexpr int ELL_OPT = 5;         // first slot gathered only when it holds an entry
 
 enum : int {
   S_RUN = 0,
@@ -469,12 +471,67 @@ __global__ void __launch_bounds__(Map<KP>::NT)
 // A finished slot takes the next column (slot order), or retires when none is
 // left; its results go out now, a retired slot's x at the final harvest.
 struct Sched {
-  int* slot_col;  // column in each slot, -1 = none
-  int* retired;   // 1 = finished, nothing left to take, x not yet harvested
-  int* next;      // next column to hand out
-  int* nfin;      // finished columns (harvested or retired); the host stops at ncols
+  int* slot_col;     // column in each slot, -1 = none
+  int* retired;      // 1 = finished, nothing left to take, x not yet harvested
+  int* next;         // next position of `order` to hand out
+  int* nfin;         // finished columns (harvested or retired); the host stops at ncols
+  const int* order;  // hand-out order of the columns (longest expected first)
   int ncols;
 };
+
+// Hand-out order.  A slot idles once no column is left, so the columns that need
+// the most iterations should start first.  Jacobi-preconditioned CG takes longest
+// on smooth right-hand sides, whose Rayleigh quotient b'Ab / b'Db is small (C3:
+// Spearman -0.74 against the iteration counts, tools/order_probe.py), so columns
+// go out in ascending b'Ab / b'Db.  Only the schedule changes: a column's
+// arithmetic does not depend on its slot or start time.  Per block b: partial
+// sums over rows 16 b, 16 (b + G), ... of b_i (A b)_i and d_i b_i^2 for every column
+// (thread t owns columns t, t + NT, ...), in shared memory; k_col_rq_sum adds the
+// G partials per column in block order (deterministic).
+constexpr int RQ_NT = 256, RQ_MAXC = 2048;
+constexpr int RQ_STRIDE = 16;  // every 16th row: an estimate is enough to order columns
+__global__ void __launch_bounds__(RQ_NT)
+    k_col_rq(int n, const int* __restrict__ eci, const double* __restrict__ ecv, const int32_t* __restrict__ indptr,
+             const int32_t* __restrict__ indices, const double* __restrict__ val, const double* __restrict__ d,
+             const double* __restrict__ B, int ldb, int ncols, double* part) {
+  __shared__ double s_num[RQ_MAXC], s_den[RQ_MAXC];
+  for (int c = threadIdx.x; c < ncols; c += RQ_NT) s_num[c] = s_den[c] = 0.0;
+  for (int i = blockIdx.x * RQ_STRIDE; i < n; i += gridDim.x * RQ_STRIDE) {
+    const int c0 = __ldg(eci + (size_t)i * ELL_W);
+    const bool lng = (c0 & ELL_LONG) != 0;
+    const double di = d[i];
+    for (int c = threadIdx.x; c < ncols; c += RQ_NT) {
+      double ab = 0.0;
+#pragma unroll
+      for (int e = 0; e < ELL_W; ++e) {
+        const int ce = __ldg(eci + (size_t)i * ELL_W + e) & (ELL_LONG - 1);
+        if (e >= ELL_OPT && __ldg(eci + (size_t)i * ELL_W + e) < 0) continue;
+        ab = __fma_rn(__ldg(ecv + (size_t)i * ELL_W + e), __ldg(B + (size_t)ce * ldb + c), ab);
+      }
+      if (lng)
+        for (int j = indptr[i] + ELL_W; j < indptr[i + 1]; ++j)
+          ab = __fma_rn(val[j], __ldg(B + (size_t)indices[j] * ldb + c), ab);
+      const double bi = __ldg(B + (size_t)i * ldb + c);
+      s_num[c] = __fma_rn(bi, ab, s_num[c]);
+      s_den[c] = __fma_rn(di * bi, bi, s_den[c]);
+    }
+  }
+  for (int c = threadIdx.x; c < ncols; c += RQ_NT) {
+    part[(size_t)blockIdx.x * 2 * ncols + c] = s_num[c];
+    part[(size_t)blockIdx.x * 2 * ncols + ncols + c] = s_den[c];
+  }
+}
+
+__global__ void k_col_rq_sum(int nblocks, int ncols, const double* __restrict__ part, double* rq) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= ncols) return;
+  double num = 0.0, den = 0.0;
+  for (int b = 0; b < nblocks; ++b) {
+    num += part[(size_t)b * 2 * ncols + c];
+    den += part[(size_t)b * 2 * ncols + ncols + c];
+  }
+  rq[c] = den > 0.0 ? num / den : INFINITY;  // b = 0: last (it finishes at once)
+}
 
 // Tail compaction.  Once no column is left to hand out, finished slots leave
 // holes and the kernels keep moving every lane that still holds a running
@@ -605,9 +662,9 @@ __global__ void __launch_bounds__(Map<KP>::NT)
   if (tid < KP) {
     int rank = 0;
     for (int i = 0; i < tid; ++i) rank += s_take[i];
-    const int col = nx + rank;
-    s_ref[tid] = (take && col < sc.ncols) ? col : -1;
-    s_harv[tid] = (take && col < sc.ncols) ? sc.slot_col[tid] : -1;
+    const int pos = nx + rank;
+    s_ref[tid] = (take && pos < sc.ncols) ? sc.order[pos] : -1;
+    s_harv[tid] = (take && pos < sc.ncols) ? sc.slot_col[tid] : -1;
     refill = s_ref[tid] >= 0;
   }
   const int nref = __syncthreads_count(refill);
@@ -702,8 +759,6 @@ __global__ void __launch_bounds__(Map<KP>::NT)
 // 0's column; their entries 8.. come from the CSR.  Sum order, for every kp:
 // slots 7..0, then entries 8.. in order.  A/B timings of the variants are in
 // DESIGN.md §3.
-constexpr int ELL_LONG = 1 << 30;
-constexpr int ELL_OPT = 5;  // first slot gathered only when it holds an entry
 constexpr int ELL_HB = 4;   // gathers in flight per batch
 
 __global__ void k_ell_fill(int n, const int32_t* __restrict__ indptr,
@@ -1625,6 +1680,11 @@ int run_stream(const hf_csr* A, const double* d, const double* Ball, int ldb, in
   hv.true_res = cv.take<double>(ncols);
   hv.best_res = cv.take<double>(ncols);
   Sched sched;
+  int* d_order = cv.take<int>(ncols);
+  const bool ordered = ncols > KP && ncols <= RQ_MAXC;
+  double* rq_part = ordered ? cv.take<double>((size_t)GRID * 2 * ncols) : nullptr;
+  double* rq = ordered ? cv.take<double>(ncols) : nullptr;
+  sched.order = d_order;
   sched.slot_col = cv.take<int>(2 * KP + 2);  // slot_col, retired, next, nfin: one block
   sched.retired = sched.slot_col + KP;
   sched.next = sched.slot_col + 2 * KP;
@@ -1655,13 +1715,28 @@ int run_stream(const hf_csr* A, const double* d, const double* Ball, int ldb, in
   HF_CUDA(cudaMemsetAsync(L.xmask, 0, sizeof(int) * (XD + 1) * KP, stream));
   HF_CUDA(cudaMemsetAsync(L.summary, 0, sizeof(int) * SUM_N, stream));
   HF_CUDA(cudaMemsetAsync(L.state, 0, sizeof(int) * KP, stream));
-  // first fill: slot j <- column j (b = 0 and state ZERO for slots beyond ncols)
+  // hand-out order: ascending Rayleigh quotient (longest expected first), ties by index
+  std::vector<int> order(ncols);
+  for (int j = 0; j < ncols; ++j) order[j] = j;
+  if (ordered) {
+    k_col_rq<<<GRID, RQ_NT, 0, stream>>>(n, g.ell.ci, g.ell.cv, A->indptr, A->indices, A->val, d, Ball, ldb,
+                                         ncols, rq_part);
+    k_col_rq_sum<<<(ncols + 255) / 256, 256, 0, stream>>>(GRID, ncols, rq_part, rq);
+    HF_LAUNCH_CHECK();
+    count_launches(2);
+    std::vector<double> h_rq(ncols);
+    HF_CUDA(cudaMemcpyAsync(h_rq.data(), rq, sizeof(double) * ncols, cudaMemcpyDeviceToHost, stream));
+    HF_CUDA(cudaStreamSynchronize(stream));
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return h_rq[a] < h_rq[b]; });
+  }
+  HF_CUDA(cudaMemcpyAsync(d_order, order.data(), sizeof(int) * ncols, cudaMemcpyHostToDevice, stream));
+  // first fill: slot j <- order[j] (b = 0 and state ZERO for slots beyond ncols)
   SlotLists sl;
   std::vector<int> ctl(2 * KP + 2, 0);  // slot_col, retired, next, nfin
   for (int j = 0; j < 64; ++j) sl.refill[j] = sl.harvest[j] = -1;
   for (int j = 0; j < KP; ++j) {
-    sl.refill[j] = j < ncols ? j : -2;
-    ctl[j] = j < ncols ? j : -1;
+    sl.refill[j] = j < ncols ? order[j] : -2;
+    ctl[j] = j < ncols ? order[j] : -1;
   }
   ctl[2 * KP] = std::min(KP, ncols);
   HF_CUDA(cudaMemcpyAsync(sched.slot_col, ctl.data(), sizeof(int) * ctl.size(), cudaMemcpyHostToDevice, stream));
@@ -1728,6 +1803,11 @@ inline size_t stream_bytes(int n, int kp, int ncols) {
   cv.take<double>((size_t)n * kp);
   for (int q = 0; q < 3; ++q) cv.take<int>(ncols);
   for (int q = 0; q < 2; ++q) cv.take<double>(ncols);
+  cv.take<int>(ncols);
+  if (ncols > kp && ncols <= RQ_MAXC) {
+    cv.take<double>((size_t)GRID * 2 * ncols);
+    cv.take<double>(ncols);
+  }
   cv.take<int>(2 * kp + 2);
   return cv.used + 512;
 }
