@@ -145,7 +145,10 @@ int hf_pcg_multi(const hf_csr* A, const double* d, const double* B, int32_t n, i
  * row-major, columns 0..ncols-1) through kp slots.  When a slot's column finishes,
  * its x goes to column j of X (device n x ldb) and the slot takes the next column
  * at the next chunk boundary, so no slot waits for the slowest column of a batch.
- * Per-column iterates are bit-identical to hf_pcg_multi's (canonical reductions).
+ * Columns are handed out longest-expected-first (ascending b'Ab / b'Db, estimated
+ * on a row sample) and slots are scheduled on the device; neither changes a column's
+ * arithmetic: per-column iterates are bit-identical to hf_pcg_multi's (canonical
+ * reductions).
  * iters, status, best_iter (int32) and true_res, best_res (double): host, ncols
  * each.  FAILED columns hold x at max_iter: replay them with hf_pcg_multi and
  * freeze_at = best_iter for the best iterate (solver.py:92-93, 108-111).
